@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the SharedKVPool compress/inject hot path on B200.
+
+One step = compress every layer of a synthetic KV dump into the packed pool
+(one pkv_encode launch: q8_0 keys + FWHT/RMS/3-bit Lloyd-Max packed values)
++ materialise every layer back to bf16 for one agent (one pkv_decode launch).
+That is the reference's build_pool + inject_all round trip
+(kvpool/pool.py:258-293, :239-255). metric = algorithmic bytes / time (GB/s).
+
+Secondary: shared-pool decode attention over the packed pool for all agents
+(pkv_decode_attention, one launch pair per layer), reported as tokens/s.
+
+    python bench.py [--gpus N --steps K --warmup W --config c3 --dtype bf16]
+    python bench.py --impl reference ...   # the reference algorithm on host cores
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (layers, kv_heads, head_dim, seq_len, agents, group, description)
+    "c1": (24, 32, 64, 600, 3, 1, "SmolLM2-1.7B-shape KV (L24 H32 d64), T=600, 3 agents"),
+    "c2": (24, 32, 64, 1851, 5, 1, "SmolLM2-1.7B-shape KV (L24 H32 d64), T=1851, 5 agents"),
+    "c3": (32, 8, 128, 4096, 15, 4, "Llama-3-8B-shape KV (L32 H8 d128 GQA g4), T=4096, 15 agents"),
+    "c4": (32, 8, 128, 7194, 15, 4, "Llama-3-8B-shape KV (L32 H8 d128 GQA g4), T=7194, 15 agents"),
+}
+METRIC = "KV compress+dequant GB/s (HBM roofline); shared-pool decode tok/s"
+
+
+def algorithmic_bytes(L, H, D, T, in_bytes, out_bytes, k_mode="tensor"):
+    """per-element bytes of compress and materialise."""
+    n = H * T * D
+    vecs = H * T
+    k_scale_b = 4 if k_mode == "tensor" else 2 * ((n + 31) // 32)
+    comp = L * (n * in_bytes + n + k_scale_b + n * in_bytes + 3 * n / 8 + 4 * vecs)
+    deq = L * (n + k_scale_b + n * out_bytes + 3 * n / 8 + 4 * vecs + n * out_bytes)
+    return comp, deq
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on host cores
+# ---------------------------------------------------------------------------
+def _cpu_layer(args):
+    L_index, H, D, T, seed = args
+    import numpy as np
+
+    from oracle import kvpool_oracle as O
+
+    rng = np.random.default_rng(seed + L_index)
+    std = float(np.sqrt(1.0 / D))
+    k = rng.normal(0.0, std, size=(1, H, T, D)).astype(np.float32)
+    v = rng.normal(0.0, std, size=(1, H, T, D)).astype(np.float32)
+    t0 = time.perf_counter()
+    s, kc = O.quantize_k_tensor(k)
+    vc, vs = O.quantize_v(v)
+    O.decode_layer(kc, s, vc, vs, 16)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_step(H, D, T, layers, procs, pool=None):
+    """One bounded sample: `layers` layers, one per process, reference semantics
+    (quantize_k + quantize_v + 16-bit get_kv_for_layer). Returns seconds."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    work = [(i, H, D, T, 0) for i in range(layers)]
+    t0 = time.perf_counter()
+    if pool is None:
+        with ProcessPoolExecutor(max_workers=procs) as ex:
+            list(ex.map(_cpu_layer, work))
+    else:
+        list(pool.map(_cpu_layer, work))
+    return time.perf_counter() - t0
+
+
+def run_reference(args, cfg):
+    L, H, D, T, agents, group, desc = cfg
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from concurrent.futures import ProcessPoolExecutor
+
+    procs = os.cpu_count() or 1
+    sample_layers = procs  # one layer per host core per step
+    in_b, out_b = (2, 2) if args.dtype == "bf16" else (4, 2)
+    comp, deq = algorithmic_bytes(1, H, D, T, in_b, out_b)
+    per_layer = comp + deq
+    with ProcessPoolExecutor(max_workers=procs) as ex:
+        for _ in range(args.warmup):
+            cpu_reference_step(H, D, T, sample_layers, procs, ex)
+        times = [cpu_reference_step(H, D, T, sample_layers, procs, ex) for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = per_layer * sample_layers / sec / 1e9
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (numpy)", "data": "synthetic",
+        "config": {"workload": desc, "sample": f"{sample_layers} layers per step (one per core)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": f"{sample_layers} x 1 layer [1,{H},{T},{D}] quantize_k+quantize_v+decode16"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_24971_b200 as pk
+    from paper_2604_24971_b200 import _codec
+    from paper_2604_24971_b200.attention import decode_attention
+    from paper_2604_24971_b200.pool import _Arena, _encode_layers, raise_for_status
+
+    L, H, D, T, agents, group, desc = cfg
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    in_b = 2 if dtype == torch.bfloat16 else 4
+    g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
+    dump = pk.synth_gaussian_dump(g, seed=rank, device=dev, dtype=dtype, generator="torch")
+    ks = [k for k, _ in dump.layers]
+    vs = [v for _, v in dump.layers]
+    arena = _Arena(g, L, args.k_mode, dev)
+    kb, vb, _ = _encode_layers(ks, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena)
+    pool = pk.SharedPool(g, list(zip(kb, vb))).seal()
+    out_k = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    out_v = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    stream = torch.cuda.current_stream(dev)
+
+    def encode():
+        _encode_layers(ks, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
+
+    def decode():
+        _codec.decode(num_vectors=g.vectors_per_tensor, head_dim=D, out_dtype=torch.bfloat16,
+                      k_mode=pk.keyquant.K_MODES[args.k_mode], k_codes=pool.k_codes, k_scale=pool.k_scale,
+                      k_bscale=pool.k_bscale, v_packed=pool.v_packed, v_scales=pool.v_scales,
+                      centroids=pk.GAUSSIAN_3BIT.centroids, sign_seed=None, k_out=out_k, v_out=out_v,
+                      device=dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(args.warmup):
+        encode()
+        decode()
+    raise_for_status(arena.status)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    marks = [(ev(), ev(), ev()) for _ in range(args.steps)]
+    start, end = ev(), ev()
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize(dev)
+        start.record(stream)
+        for a, b, c in marks:
+            a.record(stream)
+            encode()
+            b.record(stream)
+            decode()
+            c.record(stream)
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    total_ms = start.elapsed_time(end)
+    enc_ms = sum(a.elapsed_time(b) for a, b, _ in marks) / args.steps
+    dec_ms = sum(b.elapsed_time(c) for _, b, c in marks) / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    comp_b, deq_b = algorithmic_bytes(L, H, D, T, in_b, 2, args.k_mode)
+    value = world * (comp_b + deq_b) / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.skip_e2e:
+        host_layers = [(k.values.cpu().pin_memory(), v.values.cpu().pin_memory()) for k, v in dump.layers]
+        host_dump = pk.KvDump(g, tuple((pk.KvTensor(g, k), pk.KvTensor(g, v)) for k, v in host_layers))
+        host_out = [(torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory(),
+                     torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in range(L)]
+
+        def e2e_step():
+            p = pk.build_pool(host_dump, build_stats=False, device=dev)
+            view = p.attach(16)
+            for (hk, hv), (dk, dv) in zip(host_out, view.materialize_all()):
+                hk.copy_(dk, non_blocking=True)
+                hv.copy_(dv, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        es, ee = ev(), ev()
+        n_e2e = max(1, min(args.steps, 5))
+        es.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        ee.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = es.elapsed_time(ee) / n_e2e
+        h2d = 2 * L * g.elements_per_tensor * in_b
+        d2h = 2 * L * g.elements_per_tensor * 2
+        e2e = {"value": world * (comp_b + deq_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    # ---- shared-pool decode attention (all agents, all layers) ----
+    attn = None
+    if not args.skip_attention and D in (64, 128):
+        q = torch.randn(agents, H, group, D, device=dev, dtype=torch.bfloat16)
+        outa = torch.empty_like(q)
+        need = pk._lib.load().pkv_attention_workspace_bytes(agents, H, group, D, T)
+        ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=dev)
+
+        def attn_step():
+            for li in range(L):
+                decode_attention(pool, li, q, softmax_scale=D ** -0.5, out=outa, workspace=ws)
+
+        for _ in range(2):
+            attn_step()
+        torch.cuda.synchronize(dev)
+        s2, e2 = ev(), ev()
+        s2.record(stream)
+        for _ in range(args.steps):
+            attn_step()
+        e2.record(stream)
+        torch.cuda.synchronize(dev)
+        a_ms = s2.elapsed_time(e2) / args.steps
+        pool_bytes = L * (g.elements_per_tensor * (1 + 3 / 8) + 4 * g.vectors_per_tensor + 4)
+        attn = {"tokens_per_s": world * agents / (a_ms / 1e3), "ms_per_token_step": a_ms,
+                "agents": agents, "layers": L, "scope": "attention only (all layers), batched agents",
+                "pool_gbs": pool_bytes / (a_ms / 1e3) / 1e9}
+
+    peak, peak_kind = measured_peaks()
+    dom_ms, dom_bytes, dom_name = (enc_ms, comp_b, "encode_kernel") if enc_ms >= dec_ms else (dec_ms, deq_b, "decode_kernel")
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    prof = ROOT / "profiles" / "traffic.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"{args.config}/{args.dtype}/{dom_name}")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and not args.skip_cpu:
+        from concurrent.futures import ProcessPoolExecutor
+
+        procs = os.cpu_count() or 1
+        with ProcessPoolExecutor(max_workers=procs) as ex:
+            cpu_reference_step(H, D, T, min(procs, 2), procs, ex)  # warm the workers
+            sec = cpu_reference_step(H, D, T, procs, procs, ex)
+        cb, dbb = algorithmic_bytes(1, H, D, T, in_b, 2)
+        cpu = {"value": (cb + dbb) * procs / sec / 1e9, "unit": "GB/s", "cores": procs, "kind": "port",
+               "sample": f"{procs} layers [1,{H},{T},{D}] (one per process): quantize_k+quantize_v+decode16"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 in / u8+int8 pool / bf16 out" if in_b == 2 else "f32 in / u8+int8 pool / bf16 out",
+            "data": "synthetic (torch.randn, var 1/head_dim, random-init)",
+            "config": {"workload": desc, "layers": L, "kv_heads": H, "head_dim": D, "seq_len": T,
+                       "agents": agents, "k_scale_mode": args.k_mode,
+                       "step": "build_pool (pkv_encode, all layers) + inject_all to bf16 (pkv_decode, all layers)",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "parallelism": f"replica x{world} (independent pools per GPU)"},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic},
+            "kernels": {"encode_ms": enc_ms, "encode_gbs": comp_b / (enc_ms / 1e3) / 1e9,
+                        "decode_ms": dec_ms, "decode_gbs": deq_b / (dec_ms / 1e3) / 1e9,
+                        "encode_bytes": comp_b, "decode_bytes": deq_b},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "decode_attention": attn,
+            "replayed_vectors_per_build": pool.replay_count,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--k-mode", default="tensor", choices=["tensor", "block32"])
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-attention", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

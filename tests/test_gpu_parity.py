@@ -1,0 +1,239 @@
+"""Parity of the sm_100a codec (through the C ABI) with the oracle / reference goldens.
+
+Bar: bit-exact codes, scales, packed bytes and decoded K/V (f32 and bf16);
+attention within 1e-3 relative of an fp64 oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_24971_b200 as pk
+from oracle import kvpool_oracle as O
+from pkv_testutil import golden_case
+
+pytestmark = pytest.mark.gpu
+
+POOL_CASES = ["c1mini", "d128", "d128_sign", "d64_batch2", "d8", "d16", "d32", "d256", "bf16in", "laplace"]
+
+
+def u32(t):
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        return (t.view(torch.int16).numpy().astype(np.uint16).astype(np.uint32) << 16)
+    return t.float().numpy().view(np.uint32)
+
+
+def dump_from_golden(golden, name, dtype=torch.float32):
+    c = golden_case(golden, name)
+    g = pk.ModelGeometry(num_layers=c["L"], kv_heads=c["H"], head_dim=c["D"], seq_len=c["T"], batch=c["B"])
+    layers = []
+    for li in range(c["L"]):
+        k = torch.from_numpy(golden[f"{name}/k_in/{li}"]).cuda().to(dtype)
+        v = torch.from_numpy(golden[f"{name}/v_in/{li}"]).cuda().to(dtype)
+        layers.append((pk.KvTensor(g, k), pk.KvTensor(g, v)))
+    return c, pk.KvDump(g, tuple(layers))
+
+
+@pytest.mark.parametrize("name", POOL_CASES)
+def test_build_pool_bit_exact_vs_reference(golden, name):
+    c, dump = dump_from_golden(golden, name)
+    pool = pk.build_pool(dump, sign_seed=c["sign_seed"])
+    for li in range(c["L"]):
+        kq, vq = pool.layer_blocks(li)
+        assert kq.scale == float(golden[f"{name}/k_scale/{li}"][0])
+        assert np.array_equal(kq.codes.cpu().numpy(), golden[f"{name}/k_codes/{li}"])
+        assert np.array_equal(vq.codes.cpu().numpy(), golden[f"{name}/v_codes/{li}"])
+        assert np.array_equal(vq.packed.cpu().numpy(), golden[f"{name}/v_packed/{li}"])
+        assert np.array_equal(u32(vq.scales), golden[f"{name}/v_scales/{li}"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", POOL_CASES)
+@pytest.mark.parametrize("bits", [16, 32])
+def test_get_kv_for_layer_bit_exact(golden, name, bits):
+    c, dump = dump_from_golden(golden, name)
+    pool = pk.build_pool(dump, sign_seed=c["sign_seed"])
+    view = pool.attach(bits)
+    for li in range(c["L"]):
+        k, v = view.get_kv_for_layer(li)
+        assert k.values.dtype == (torch.bfloat16 if bits == 16 else torch.float32)
+        assert np.array_equal(u32(k.values), golden[f"{name}/k{bits}/{li}"].view(np.uint32))
+        assert np.array_equal(u32(v.values), golden[f"{name}/v{bits}/{li}"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["c1mini", "d128_sign", "d8"])
+def test_inject_all_transcript_matches_reference(golden, name):
+    c, dump = dump_from_golden(golden, name)
+    pool = pk.build_pool(dump, sign_seed=c["sign_seed"])
+    tr = pool.attach(16).inject_all()
+    assert np.array_equal(np.array(tr.checksums(), dtype=np.uint64), golden[f"{name}/checksums16"])
+
+
+def test_bf16_inputs_give_reference_codes(golden):
+    # bf16 device inputs (exactly the bf16-rounded values of the golden case)
+    c, dump = dump_from_golden(golden, "bf16in", dtype=torch.bfloat16)
+    pool = pk.build_pool(dump)
+    for li in range(c["L"]):
+        kq, vq = pool.layer_blocks(li)
+        assert kq.scale == float(golden[f"bf16in/k_scale/{li}"][0])
+        assert np.array_equal(kq.codes.cpu().numpy(), golden[f"bf16in/k_codes/{li}"])
+        assert np.array_equal(vq.codes.cpu().numpy(), golden[f"bf16in/v_codes/{li}"])
+        assert np.array_equal(u32(vq.scales), golden[f"bf16in/v_scales/{li}"].view(np.uint32))
+
+
+def test_value_threshold_ties(golden):
+    x = golden["tie/v_in"]
+    g = pk.ModelGeometry(num_layers=1, kv_heads=1, head_dim=128, seq_len=64)
+    vq = pk.quantize_v(pk.KvTensor(g, torch.from_numpy(x).cuda()))
+    assert np.array_equal(vq.codes.cpu().numpy(), golden["tie/v_codes"])
+    assert np.array_equal(u32(vq.scales), golden["tie/v_scales"].view(np.uint32))
+
+
+@pytest.mark.parametrize("kat", ["sym", "grid", "half", "halfgrid_all"])
+def test_key_known_answers(golden, kat):
+    vals = golden[f"kat/{kat}/in"]
+    g = pk.ModelGeometry(num_layers=1, kv_heads=1, head_dim=1, seq_len=vals.size)
+    kq = pk.quantize_k(pk.KvTensor(g, torch.from_numpy(vals.reshape(1, 1, -1, 1)).cuda()))
+    assert kq.scale == float(golden[f"kat/{kat}/scale"][0])
+    assert np.array_equal(kq.codes.cpu().numpy().reshape(-1), golden[f"kat/{kat}/codes"])
+
+
+def test_key_half_point_adversaries():
+    # values at exact (n + 1/2) * s for many n with a non-power-of-two scale:
+    # the fp32 fast path must hand these to the exact path
+    rng = np.random.default_rng(11)
+    peak = np.float32(1.7)
+    s = np.float32(peak / 127)
+    n = rng.integers(-126, 126, size=20000)
+    vals = ((n + 0.5) * np.float64(s)).astype(np.float32)
+    vals = np.concatenate([vals, np.nextafter(vals, np.float32(np.inf)), np.nextafter(vals, np.float32(-np.inf)),
+                           [peak]]).astype(np.float32)
+    g = pk.ModelGeometry(num_layers=1, kv_heads=1, head_dim=1, seq_len=vals.size)
+    kq = pk.quantize_k(pk.KvTensor(g, torch.from_numpy(vals.reshape(1, 1, -1, 1)).cuda()))
+    scale, want = O.quantize_k_tensor(vals.reshape(1, 1, -1, 1))
+    assert kq.scale == scale
+    assert np.array_equal(kq.codes.cpu().numpy(), want)
+
+
+def test_full_config1_shape_bit_exact():
+    # BASELINE configs[0]: SmolLM2 shape L24 H32 d64 T600, seed 0, full size
+    g = pk.ModelGeometry(num_layers=24, kv_heads=32, head_dim=64, seq_len=600)
+    layers = O.synth_dump(24, 32, 64, 600, seed=0)
+    dump = pk.KvDump(g, tuple((pk.KvTensor(g, torch.from_numpy(k).cuda()),
+                               pk.KvTensor(g, torch.from_numpy(v).cuda())) for k, v in layers))
+    pool = pk.build_pool(dump)
+    view = pool.attach(16)
+    decoded = view.materialize_all()
+    for li in (0, 7, 23):
+        k, v = layers[li]
+        scale, kc = O.quantize_k_tensor(k)
+        vc, vs = O.quantize_v(v)
+        kq, vq = pool.layer_blocks(li)
+        assert kq.scale == scale and np.array_equal(kq.codes.cpu().numpy(), kc)
+        assert np.array_equal(vq.codes.cpu().numpy(), vc)
+        assert np.array_equal(u32(vq.scales), vs.view(np.uint32))
+        kd, vd = O.decode_layer(kc, scale, vc, vs, 16)
+        assert np.array_equal(u32(decoded[li][0]), kd.view(np.uint32))
+        assert np.array_equal(u32(decoded[li][1]), vd.view(np.uint32))
+    from fractions import Fraction
+    assert Fraction(g.baseline_cache_nbytes() * 8, pool.logical_payload_bits()) == Fraction(32, 11)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_block32_keys_match_restatement(d):
+    rng = np.random.default_rng(d)
+    x = rng.normal(0, 0.2, size=(1, 4, 77, d)).astype(np.float32)
+    x[0, 1, 3, :] *= 1e-3
+    x[0, 2, 5, :32] = 0.0
+    g = pk.ModelGeometry(num_layers=1, kv_heads=4, head_dim=d, seq_len=77)
+    kq = pk.quantize_k(pk.KvTensor(g, torch.from_numpy(x).cuda()), k_scale_mode="block32")
+    s16, codes = O.quantize_k_block32(x)
+    assert np.array_equal(kq.block_scales.cpu().numpy().view(np.uint16), s16.view(np.uint16))
+    assert np.array_equal(kq.codes.cpu().numpy(), codes)
+    back = pk.dequantize_k(kq).values.cpu().numpy()
+    assert np.array_equal(back.view(np.uint32), O.dequantize_k_block32(codes, s16).view(np.uint32))
+
+
+def test_large_shape_properties():
+    # Llama-3-8B layer shape at 4K tokens through the whole path; properties that
+    # hold at any size: key error <= s/2, value NMSE ~ 0.0345, determinism,
+    # pool bytes O(1) in agents, idempotent requantisation of decoded keys.
+    g = pk.ModelGeometry(num_layers=2, kv_heads=8, head_dim=128, seq_len=4096)
+    dump = pk.synth_gaussian_dump(g, seed=0, device="cuda", generator="torch", dtype=torch.bfloat16)
+    p1 = pk.build_pool(dump, build_stats=True)
+    p2 = pk.build_pool(dump, build_stats=False)
+    for li in range(2):
+        k1, v1 = p1.layer_blocks(li)
+        k2, v2 = p2.layer_blocks(li)
+        assert torch.equal(k1.codes, k2.codes) and torch.equal(v1.packed, v2.packed)
+        assert torch.equal(v1.scales, v2.scales)
+        st = p1.build_stats[li]
+        assert st.k_max_err <= st.k_scale / 2 * (1 + 1e-6)
+        assert abs(st.v_nmse - 0.0345) < 0.002
+    before = p1.payload_nbytes()
+    for _ in range(15):
+        p1.attach(16).materialize_all()
+    assert p1.payload_nbytes() == before
+    kd = pk.dequantize_k(p1.layer_blocks(0)[0])
+    kq2 = pk.quantize_k(kd)
+    assert torch.equal(kq2.codes, p1.layer_blocks(0)[0].codes)
+
+
+def test_nonfinite_input_raises_geometry_error():
+    g = pk.ModelGeometry(num_layers=2, kv_heads=2, head_dim=64, seq_len=8)
+    dump = pk.synth_gaussian_dump(g, seed=1, device="cuda")
+    dump.layers[1][1].values[0, 1, 2, 3] = float("nan")
+    with pytest.raises(pk.GeometryError, match="NaN or Inf"):
+        pk.build_pool(dump)
+    dump = pk.synth_gaussian_dump(g, seed=1, device="cuda")
+    dump.layers[0][0].values[0, 0, 0, 0] = float("inf")
+    with pytest.raises(pk.GeometryError, match="NaN or Inf"):
+        pk.build_pool(dump)
+
+
+def test_views_are_bit_identical_and_transcripts_agree():
+    g = pk.ModelGeometry(num_layers=3, kv_heads=2, head_dim=32, seq_len=16)
+    pool = pk.build_pool(pk.synth_gaussian_dump(g, seed=20, device="cuda"))
+    a, b = pool.attach(), pool.attach()
+    assert a.agent_id != b.agent_id
+    assert a.inject_all().checksums() == b.inject_all().checksums()
+    with pytest.raises(IndexError):
+        a.get_kv_for_layer(3)
+
+
+def test_packed_snapshot_roundtrip(tmp_path, golden):
+    c, dump = dump_from_golden(golden, "d128_sign")
+    pool = pk.build_pool(dump, sign_seed=c["sign_seed"])
+    for packed in (False, True):
+        path = tmp_path / f"p{int(packed)}.pkvp"
+        pk.save_pool(pool, path, packed=packed)
+        back = pk.load_pool(path)
+        assert back.sign_seed == c["sign_seed"]
+        for li in range(c["L"]):
+            (k1, v1), (k2, v2) = pool.decode_layers([li])[0], back.decode_layers([li])[0]
+            assert torch.equal(k1, k2) and torch.equal(v1, v2)
+
+
+def test_decode_attention_matches_fp64_oracle():
+    from paper_2604_24971_b200 import attention as A
+
+    g = pk.ModelGeometry(num_layers=1, kv_heads=8, head_dim=128, seq_len=1000)
+    dump = pk.synth_gaussian_dump(g, seed=3, device="cuda")
+    pool = pk.build_pool(dump, build_stats=False)
+    R, G = 15, 4
+    q = torch.randn(R, 8, G, 128, device="cuda")
+    tail_len = torch.randint(0, 9, (R,), device="cuda", dtype=torch.int32)
+    tk = torch.randn(R, 8, 8, 128, device="cuda").bfloat16()
+    tv = torch.randn(R, 8, 8, 128, device="cuda").bfloat16()
+    out = A.decode_attention(pool, 0, q, tail_k=tk, tail_v=tv, tail_len=tail_len,
+                             softmax_scale=128 ** -0.5, out_dtype=torch.float32)
+    (kd, vd), = pool.decode_layers([0], torch.float32)
+    tails_k = [tk[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
+    tails_v = [tv[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
+    want = O.attention_over_pool(q.cpu().numpy(), kd[0].cpu().numpy(), vd[0].cpu().numpy(), 128 ** -0.5,
+                                 tails_k, tails_v)
+    got = out.cpu().numpy().astype(np.float64)
+    rel = np.abs(got - want).max() / np.abs(want).max()
+    assert rel < 1e-3, rel
