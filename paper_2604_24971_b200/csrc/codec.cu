@@ -20,6 +20,12 @@
 //            boundary, or any of whose normalised coordinates lies within a
 //            proven error bound `delta` of a decision threshold, is replayed
 //            warp-cooperatively in fp64 in numpy's exact operation order.
+//
+// Work decomposition: every kernel runs a static, warp-granular schedule
+// (no block barriers); the encode kernel is launched cooperatively so that
+// all warps are co-resident, which makes its one cross-warp dependency (keys
+// of layer l wait for layer l's absmax) deadlock-free without atomics on a
+// ticket counter.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -33,25 +39,29 @@ struct Codebook3 {
   float mid32[7];
   float cent32[8];
   double mid64[7];
+  int symmetric;
 };
+
+constexpr int kMaxRounds = kMaxLayers + 16;
 
 struct EncodeArgs {
   int num_layers;
   int head_dim;
   int k_mode;
-  int do_k, do_v;
-  int use_sign;
-  int vec_ok;               // all pointers aligned and n % 8 == 0
-  long long nvec;           // vectors per layer
-  long long nelem;          // elements per layer
-  int a_items, e_items, v_items;  // per layer
+  int vec_ok;                     // all pointers aligned and n % 8 == 0
+  long long nvec;                 // vectors per layer
+  long long nelem;                // elements per layer
+  int a_items, e_items, v_items;  // warp items per layer
+  int lag;                        // key-encode of layer l runs in round l + lag
+  int num_rounds;
+  long long round_start[kMaxRounds + 1];
   long long total_items;
-  float delta;              // guard band on normalised coordinates
+  float delta;                    // guard band on normalised coordinates
   uint32_t sign_bits[8];
   Codebook3 cb;
-  uint32_t* status;         // [L]
-  uint32_t* replay_count;   // [1] or null
-  uint32_t* ws;             // [0] ticket, [1..L] max bits, [1+L..2L] done
+  uint32_t* status;               // [L]
+  uint32_t* replay_count;         // [1] or null
+  uint32_t* ws;                   // [0..L) max bits, [L..2L) done counters
   const void* k_in[kMaxLayers];
   const void* v_in[kMaxLayers];
   int8_t* k_codes[kMaxLayers];
@@ -65,13 +75,12 @@ struct DecodeArgs {
   int num_layers;
   int head_dim;
   int k_mode;
-  int do_k, do_v;
-  int use_sign;
   int vec_ok;
   long long nvec, nelem;
-  int k_items, v_items;  // per layer
+  int k_items, v_items;  // warp items per layer
   long long total_items;
-  float sqrt_d32;
+  float sqrt_d32;        // f32(sqrt(d))
+  float rcp_sqrt_d32;    // RN(1 / f32(sqrt(d)))
   uint32_t sign_bits[8];
   float cent32[8];
   const int8_t* k_codes[kMaxLayers];
@@ -83,16 +92,24 @@ struct DecodeArgs {
   void* v_out[kMaxLayers];
 };
 
-constexpr int kKElems = kThreads * 32;  // key elements per work item
-constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer
-constexpr float kKeyEps = 4e-5f;        // |q - n| half-point guard for keys
+constexpr int kWarps = kThreads / 32;
+constexpr int kKChunks = 32;                 // 8-element chunks per lane per key item
+constexpr int kKElems = 32 * 8 * kKChunks;   // key elements per warp item (8192)
+constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
+constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
 
 template <int D>
 struct VItem {
-  // value vectors per work item: ~32K coordinates
-  static constexpr int ITERS = (32768 / (VG<D>::VPI * D)) > 0 ? (32768 / (VG<D>::VPI * D)) : 1;
-  static constexpr int VECS = ITERS * VG<D>::VPI;
+  // value vectors per warp item: ~16K coordinates
+  static constexpr int ITERS = (16384 / (VG<D>::VPW * D)) > 0 ? (16384 / (VG<D>::VPW * D)) : 1;
+  static constexpr int VECS = ITERS * VG<D>::VPW;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // keys
@@ -109,116 +126,115 @@ __device__ __forceinline__ int key_code_exact(float x, float s, int lo, int hi) 
   return (int)r;
 }
 
-// Fast key code with exactness guard. Returns the int8 code in the low byte
-// of the result; sets `near` if the element must take the exact path.
-__device__ __forceinline__ uint32_t key_code_fast(float x, float rcp, bool clip, bool& near) {
-  float q = x * rcp;
-  if (clip) q = fminf(fmaxf(q, -200.f), 200.f);
-  float m = q + kMagic;             // RNE to an integer
-  float n = m - kMagic;
-  float diff = q - n;               // in [-0.5, 0.5]
-  near |= fabsf(diff) > (0.5f - kKeyEps);
-  int code = (int)(__float_as_uint(m) - 0x4B400000u);
-  if (clip) code = max(-127, min(127, code));
-  return (uint32_t)code & 0xffu;
+// 8 key codes of one chunk. Fast path: q = x * (1/s) rounded to nearest via
+// the 2^23 magic; the low byte of the magic sum is the two's-complement code.
+// Elements within kKeyEps of a half-point fall back to the exact formula.
+template <bool CLIP>
+__device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float rcp, bool force_exact) {
+  float m[8];
+  float worst = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float q = x[j] * rcp;
+    if (CLIP) q = fminf(fmaxf(q, -127.f), 127.f);
+    m[j] = q + kMagic;
+    const float n = m[j] - kMagic;
+    worst = fmaxf(worst, fabsf(q - n));
+  }
+  uint2 w;
+  w.x = __byte_perm(__byte_perm(__float_as_uint(m[0]), __float_as_uint(m[1]), 0x0040),
+                    __byte_perm(__float_as_uint(m[2]), __float_as_uint(m[3]), 0x0040), 0x5410);
+  w.y = __byte_perm(__byte_perm(__float_as_uint(m[4]), __float_as_uint(m[5]), 0x0040),
+                    __byte_perm(__float_as_uint(m[6]), __float_as_uint(m[7]), 0x0040), 0x5410);
+  if (force_exact || worst > 0.5f - kKeyEps) {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, CLIP ? -127 : -128, 127) & 0xffu);
+    w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+    w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
+  }
+  return w;
 }
 
-__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+// |x| bit patterns of 8 inputs, max-reduced without unpacking bf16
+__device__ __forceinline__ uint32_t chunk_absmax_bits(const float* p) {
+  const uint4 a = ld_stream_u4(p), b = ld_stream_u4(p + 4);
+  uint32_t m = max(max(a.x & 0x7fffffffu, a.y & 0x7fffffffu), max(a.z & 0x7fffffffu, a.w & 0x7fffffffu));
+  return max(m, max(max(b.x & 0x7fffffffu, b.y & 0x7fffffffu), max(b.z & 0x7fffffffu, b.w & 0x7fffffffu)));
+}
+__device__ __forceinline__ uint32_t chunk_absmax_bits(const __nv_bfloat16* p) {
+  const uint4 a = ld_stream_u4(p);
+  uint32_t m = __vmaxu2(__vmaxu2(a.x & 0x7fff7fffu, a.y & 0x7fff7fffu),
+                        __vmaxu2(a.z & 0x7fff7fffu, a.w & 0x7fff7fffu));
+  m = max(m & 0xffffu, m >> 16);
+  return m << 16;  // bf16 -> f32 bit pattern
+}
 
 template <typename TIn>
-__device__ void k_absmax_item(const EncodeArgs& a, int layer, int item, uint32_t* red) {
+__device__ void k_absmax_item(const EncodeArgs& a, int layer, int item, int lane) {
   const TIn* src = static_cast<const TIn*>(a.k_in[layer]);
   const long long e0 = (long long)item * kKElems;
   const long long n = a.nelem;
   uint32_t m = 0;
   if (a.vec_ok) {
-#pragma unroll
-    for (int i = 0; i < kKElems / (kThreads * 8); ++i) {
-      long long e = e0 + ((long long)i * kThreads + threadIdx.x) * 8;
-      if (e < n) {
-        float x[8];
-        load8(src + e, x);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) m = max(m, abs_bits(x[j]));
-      }
+#pragma unroll 8
+    for (int i = 0; i < kKChunks; ++i) {
+      const long long e = e0 + ((long long)i * 32 + lane) * 8;
+      if (e < n) m = max(m, chunk_absmax_bits(src + e));
     }
   } else {
-    for (int i = threadIdx.x; i < kKElems; i += kThreads) {
-      long long e = e0 + i;
-      if (e < n) m = max(m, abs_bits(load1(src + e)));
+    for (int i = lane; i < kKElems; i += 32) {
+      const long long e = e0 + i;
+      if (e < n) m = max(m, __float_as_uint(load1(src + e)) & 0x7fffffffu);
     }
   }
-  // block reduce
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t mm = 0;
-    for (int w = 0; w < kThreads / 32; ++w) mm = max(mm, red[w]);
-    uint32_t* maxbits = a.ws + 1;
-    uint32_t* done = a.ws + 1 + a.num_layers;
-    atomicMax(&maxbits[layer], mm);
+  if (lane == 0) {
+    atomicMax(&a.ws[layer], m);
     __threadfence();
-    atomicAdd(&done[layer], 1u);
+    atomicAdd(&a.ws[a.num_layers + layer], 1u);
   }
 }
 
-// Encode one item of keys. Per-tensor mode waits for the layer's absmax.
 template <typename TIn>
-__device__ void k_encode_item(const EncodeArgs& a, int layer, int item, uint32_t* shared_u32) {
+__device__ void k_encode_item(const EncodeArgs& a, int layer, int item, int lane) {
   const TIn* src = static_cast<const TIn*>(a.k_in[layer]);
   int8_t* dst = a.k_codes[layer];
   const long long e0 = (long long)item * kKElems;
   const long long n = a.nelem;
 
   if (a.k_mode == PKV_K_TENSOR) {
-    if (threadIdx.x == 0) {
-      volatile uint32_t* done = a.ws + 1 + a.num_layers;
-      while (done[layer] < (uint32_t)a.a_items) __nanosleep(200);
-      __threadfence();
-      volatile uint32_t* maxbits = a.ws + 1;
-      shared_u32[0] = maxbits[layer];
+    uint32_t pb = 0;
+    if (lane == 0) {
+      const uint32_t* done = a.ws + a.num_layers + layer;
+      while (ld_acquire(done) < (uint32_t)a.a_items) __nanosleep(64);
+      pb = ld_acquire(a.ws + layer);
     }
-    __syncthreads();
-    const uint32_t pb = shared_u32[0];
-    __syncthreads();
+    pb = __shfl_sync(0xffffffffu, pb, 0);
     const bool nonfinite = pb >= 0x7f800000u;
-    const float peak = __uint_as_float(pb);
-    const float s = (nonfinite || pb == 0) ? 0.f : peak / 127.0f;  // f32(peak/127)
-    if (item == 0 && threadIdx.x == 0) {
+    const float s = (nonfinite || pb == 0) ? 0.f : __uint_as_float(pb) / 127.0f;  // f32(peak/127)
+    if (item == 0 && lane == 0) {
       a.k_scale[layer][0] = s;
       if (nonfinite) atomicOr(&a.status[layer], PKV_FLAG_K_NONFINITE);
     }
     const float rcp = 1.0f / s;
-    const bool tiny = !(s >= 1e-30f);  // covers s == 0: exact path / zeros
+    const bool exact_all = !(s >= 1e-30f);  // s == 0 or tiny: exact path (zeros for s == 0)
     if (a.vec_ok) {
-#pragma unroll
-      for (int i = 0; i < kKElems / (kThreads * 8); ++i) {
-        long long e = e0 + ((long long)i * kThreads + threadIdx.x) * 8;
+#pragma unroll 4
+      for (int i = 0; i < kKChunks; ++i) {
+        const long long e = e0 + ((long long)i * 32 + lane) * 8;
         if (e >= n) continue;
         float x[8];
         load8(src + e, x);
-        bool near = tiny;
-        uint32_t c[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) c[j] = key_code_fast(x[j], rcp, false, near);
-        if (near) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, -128, 127) & 0xffu);
-        }
-        uint2 w;
-        w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-        w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-        st_u2(dst + e, w);
+        st_u2(dst + e, key_chunk<false>(x, s, rcp, exact_all));
       }
     } else {
-      for (int i = threadIdx.x; i < kKElems; i += kThreads) {
-        long long e = e0 + i;
+      for (int i = lane; i < kKElems; i += 32) {
+        const long long e = e0 + i;
         if (e >= n) continue;
-        float x = load1(src + e);
+        const float x = load1(src + e);
         dst[e] = (s == 0.f) ? (int8_t)0 : (int8_t)key_code_exact(x, s, -128, 127);
       }
     }
@@ -228,33 +244,28 @@ __device__ void k_encode_item(const EncodeArgs& a, int layer, int item, uint32_t
   // ---- block32: one fp16 scale per 32 contiguous elements (q8_0) ----
   __half* bsc = a.k_bscale[layer];
   if (a.vec_ok) {
-#pragma unroll
-    for (int i = 0; i < kKElems / (kThreads * 8); ++i) {
-      long long e = e0 + ((long long)i * kThreads + threadIdx.x) * 8;
+#pragma unroll 2
+    for (int i = 0; i < kKChunks; ++i) {
+      const long long e = e0 + ((long long)i * 32 + lane) * 8;
       const bool valid = e < n;
       float x[8];
+      uint32_t m = 0;
       if (valid) {
         load8(src + e, x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m = max(m, __float_as_uint(x[j]) & 0x7fffffffu);
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = 0.f;
       }
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m = max(m, abs_bits(x[j]));
       // 4 consecutive lanes hold one 32-element block
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
       if (!valid) continue;
       const bool nonfinite = m >= 0x7f800000u;
-      const float peak = __uint_as_float(m);
-      const float s32 = peak / 127.0f;
-      __half s16 = __float2half_rn(s32);
-      uint16_t s16b = __half_as_ushort(s16);
+      uint16_t s16b = __half_as_ushort(__float2half_rn(__uint_as_float(m) / 127.0f));
       bool overflow = false;
-      if (nonfinite) {
-        s16b = 0;
-      } else if (m == 0) {
+      if (nonfinite || m == 0) {
         s16b = 0;
       } else if ((s16b & 0x7fffu) >= 0x7c00u) {
         overflow = true;
@@ -263,35 +274,21 @@ __device__ void k_encode_item(const EncodeArgs& a, int layer, int item, uint32_t
         s16b = 1;  // peak > 0 but the scale underflows fp16: smallest subnormal
       }
       const float s = __half2float(__ushort_as_half(s16b));
-      if ((threadIdx.x & 3) == 0) {
+      if ((lane & 3) == 0) {
         bsc[e >> 5] = __ushort_as_half(s16b);
         if (nonfinite) atomicOr(&a.status[layer], PKV_FLAG_K_NONFINITE);
         if (overflow) atomicOr(&a.status[layer], PKV_FLAG_K_SCALE_OVERFLOW);
       }
-      const float rcp = 1.0f / s;
-      bool near = !(s >= 1e-30f);
-      uint32_t c[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[j] = key_code_fast(x[j], rcp, true, near);
-      if (near) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, -127, 127) & 0xffu);
-      }
-      uint2 w;
-      w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-      w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-      st_u2(dst + e, w);
+      st_u2(dst + e, key_chunk<true>(x, s, 1.0f / s, !(s >= 1e-30f)));
     }
   } else {
-    // scalar path: one thread per 32-element block
     const long long nb = (n + 31) / 32;
-    for (int bi = threadIdx.x; bi < kKElems / 32; bi += kThreads) {
-      long long b = e0 / 32 + bi;
+    for (int bi = lane; bi < kKElems / 32; bi += 32) {
+      const long long b = e0 / 32 + bi;
       if (b >= nb) continue;
-      long long lo = b * 32, hi = min(lo + 32, n);
+      const long long lo = b * 32, hi = min(lo + 32, n);
       uint32_t m = 0;
-      for (long long e = lo; e < hi; ++e) m = max(m, abs_bits(load1(src + e)));
+      for (long long e = lo; e < hi; ++e) m = max(m, __float_as_uint(load1(src + e)) & 0x7fffffffu);
       const bool nonfinite = m >= 0x7f800000u;
       uint16_t s16b = __half_as_ushort(__float2half_rn(__uint_as_float(m) / 127.0f));
       bool overflow = false;
@@ -315,19 +312,20 @@ __device__ void k_encode_item(const EncodeArgs& a, int layer, int item, uint32_t
 // Exact fp64 replay of kvpool.valuequant.quantize_v for one head vector,
 // executed by the whole warp. R: D doubles of warp scratch; C: D bytes.
 template <int D, typename TIn>
-__device__ void v_replay(const EncodeArgs& a, int layer, long long v, double* R, uint8_t* C) {
+__device__ __noinline__ void v_replay(const EncodeArgs& a, int layer, long long v, double* R,
+                                      uint8_t* C) {
   const int lane = threadIdx.x & 31;
   const TIn* p = static_cast<const TIn*>(a.v_in[layer]) + v * D;
   for (int i = lane; i < D; i += 32) {
     double x = (double)load1(p + i);
-    if (a.use_sign && sign_bit(a.sign_bits, i)) x = -x;  // vals * sign_diagonal
+    if (sign_bit(a.sign_bits, i)) x = -x;  // vals * sign_diagonal (bits are 0 without a seed)
     R[i] = x;
   }
   __syncwarp();
   for (int h = 1; h < D; h <<= 1) {  // fwht.py:31-39, in f64
     for (int q = lane; q < D / 2; q += 32) {
-      int i = (q / h) * 2 * h + (q % h);
-      double lo = R[i], hi = R[i + h];
+      const int i = (q / h) * 2 * h + (q % h);
+      const double lo = R[i], hi = R[i + h];
       R[i] = lo + hi;
       R[i + h] = lo - hi;
     }
@@ -338,14 +336,14 @@ __device__ void v_replay(const EncodeArgs& a, int layer, long long v, double* R,
   __syncwarp();
   double rms = 0.0;
   if (lane == 0) {
-    double mean = pairwise_sumsq(R, D) / (double)D;  // np.mean(np.square(rot))
+    const double mean = pairwise_sumsq(R, D) / (double)D;  // np.mean(np.square(rot))
     rms = sqrt(mean);
   }
   rms = __shfl_sync(0xffffffffu, rms, 0);
   const float scale = (float)rms;
   const double den = rms > 0.0 ? rms : 1.0;
   for (int i = lane; i < D; i += 32) {
-    double z = R[i] / den;
+    const double z = R[i] / den;
     int c = 0;
 #pragma unroll
     for (int k = 0; k < 7; ++k) c += (a.cb.mid64[k] < z) ? 1 : 0;  // searchsorted 'left'
@@ -399,7 +397,33 @@ __device__ __forceinline__ void store_words(uint8_t* p, const uint32_t (&q)[Q]) 
   }
 }
 
-// Per-warp shared memory for the value kernels.
+// Load Q packed words (inverse of store_words).
+template <int Q>
+__device__ __forceinline__ void load_words(const uint8_t* p, uint32_t (&q)[Q]) {
+  if constexpr (Q == 8) {
+    const uint2 u0 = ld_stream_u2(p), u1 = ld_stream_u2(p + 8), u2 = ld_stream_u2(p + 16);
+    q[0] = u0.x & 0xffffffu;
+    q[1] = __funnelshift_r(u0.x, u0.y, 24) & 0xffffffu;
+    q[2] = __funnelshift_r(u0.y, u1.x, 16) & 0xffffffu;
+    q[3] = u1.x >> 8;
+    q[4] = u1.y & 0xffffffu;
+    q[5] = __funnelshift_r(u1.y, u2.x, 24) & 0xffffffu;
+    q[6] = __funnelshift_r(u2.x, u2.y, 16) & 0xffffffu;
+    q[7] = u2.y >> 8;
+  } else if constexpr (Q == 4) {
+    const uint32_t u0 = ld_stream_u1(p), u1 = ld_stream_u1(p + 4), u2 = ld_stream_u1(p + 8);
+    q[0] = u0 & 0xffffffu;
+    q[1] = __funnelshift_r(u0, u1, 24) & 0xffffffu;
+    q[2] = __funnelshift_r(u1, u2, 16) & 0xffffffu;
+    q[3] = u2 >> 8;
+  } else {
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+      q[j] = (uint32_t)p[3 * j] | ((uint32_t)p[3 * j + 1] << 8) | ((uint32_t)p[3 * j + 2] << 16);
+  }
+}
+
+// Per-warp shared memory of the encode kernel.
 template <int D>
 struct VSmem {
   uint32_t stage[VG<D>::VPW][VG<D>::W + 1];  // packed-word transpose
@@ -407,20 +431,35 @@ struct VSmem {
   uint8_t C[D];
 };
 
-template <int D, typename TIn>
-__device__ void v_encode_item(const EncodeArgs& a, int layer, int item, VSmem<D>* sm_all) {
+// Lane's 64-bit sign mask over its CPT coordinates (bit c*8+e).
+template <int D>
+__device__ __forceinline__ unsigned long long lane_sign_mask(const uint32_t* bits, int s) {
   using G = VG<D>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long m = 0;
+#pragma unroll
+  for (int c = 0; c < G::NCH; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (sign_bit(bits, 8 * (s + G::TPV * c) + e)) m |= 1ull << (c * 8 + e);
+  return m;
+}
+
+template <int D, typename TIn, bool SYM, bool SIGN>
+__device__ void v_encode_item(const EncodeArgs& a, int layer, int item, int warp, int lane,
+                              VSmem<D>& sm, unsigned long long smask) {
+  using G = VG<D>;
+  static_assert(G::CPT <= 64, "sign mask holds 64 coordinates");
   const int vw = lane / G::TPV, s = lane % G::TPV;
-  VSmem<D>& sm = sm_all[warp];
   const TIn* src = static_cast<const TIn*>(a.v_in[layer]);
   uint8_t* packed = a.v_packed[layer];
   float* scales = a.v_scales[layer];
   const long long vbase = (long long)item * VItem<D>::VECS;
   const float delta = a.delta;
+  const float* m = a.cb.mid32;
 
+#pragma unroll 1
   for (int it = 0; it < VItem<D>::ITERS; ++it) {
-    const long long v = vbase + (long long)it * G::VPI + warp * G::VPW + vw;
+    const long long v = vbase + (long long)it * G::VPW + vw;
     const bool valid = v < a.nvec;
     float x[G::CPT];
     if (valid) {
@@ -436,12 +475,10 @@ __device__ void v_encode_item(const EncodeArgs& a, int layer, int item, VSmem<D>
 #pragma unroll
       for (int i = 0; i < G::CPT; ++i) x[i] = 0.f;
     }
-    if (a.use_sign) {
+    if (SIGN) {
 #pragma unroll
-      for (int c = 0; c < G::NCH; ++c)
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (sign_bit(a.sign_bits, 8 * (s + G::TPV * c) + e)) x[c * 8 + e] = -x[c * 8 + e];
+      for (int i = 0; i < G::CPT; ++i)
+        x[i] = __uint_as_float(__float_as_uint(x[i]) ^ ((uint32_t)(smask >> i) << 31));
     }
     // squared norm in fp64 from the inputs (the rotation is orthogonal):
     // every x^2 is exact in fp64, the sum is good to ~D*2^-53 relative.
@@ -451,10 +488,10 @@ __device__ void v_encode_item(const EncodeArgs& a, int layer, int item, VSmem<D>
 #pragma unroll
     for (int lb = 0; lb < G::LB; ++lb) S += __shfl_xor_sync(0xffffffffu, S, 1 << lb);
 
-    fwht_lanes<D>(x, s);
+    fwht_lanes<D>(x, s);  // U = H x (unnormalised)
 
     bool replay = false, nonfinite = false, zero = false;
-    float scale = 0.f, inv = 0.f;
+    float scale = 0.f, N = 0.f;
     if (!(S <= 1.79e308)) {
       nonfinite = true;
     } else if (S == 0.0) {
@@ -468,40 +505,65 @@ __device__ void v_encode_item(const EncodeArgs& a, int layer, int item, VSmem<D>
       const float nb = (r >= fd) ? nextafterf(scale, INFINITY) : nextafterf(scale, 0.f);
       const double half_ulp = fabs((double)nb - fd) * 0.5;
       if (half_ulp - fabs(r - fd) <= 1e-12 * r) replay = true;
-      inv = (float)rsqrt(S);  // 1/||x||; z = U/||x|| with U the unnormalised FWHT
+      N = (float)sqrt(S);  // ||x||; z = U / ||x||
     }
 
     uint32_t words[G::NCH];
-    const float* m = a.cb.mid32;
+    if (SYM) {
+      // thresholds folded into the U domain: |z| > t  <=>  |U| > t*||x||
+      const float T1 = m[4] * N, T2 = m[5] * N, T3 = m[6] * N, DL = delta * N;
+      float gmin = INFINITY, amin = INFINITY;
 #pragma unroll
-    for (int c = 0; c < G::NCH; ++c) {
-      uint32_t w = 0;
+      for (int c = 0; c < G::NCH; ++c) {
+        uint32_t w = 0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float z = x[c * 8 + e] * inv;
-        // binary search over the 7 thresholds; both boundaries of the final
-        // cell are on the search path, so the guard checks only those three.
-        const bool p1 = z > m[3];
-        const float t2 = p1 ? m[5] : m[1];
-        const bool p2 = z > t2;
-        const float t3 = p1 ? (p2 ? m[6] : m[4]) : (p2 ? m[2] : m[0]);
-        const bool p3 = z > t3;
-        replay |= (fabsf(z - m[3]) < delta) | (fabsf(z - t2) < delta) | (fabsf(z - t3) < delta);
-        const uint32_t code = (p1 ? 4u : 0u) | (p2 ? 2u : 0u) | (p3 ? 1u : 0u);
-        w |= code << (3 * e);
+        for (int e = 0; e < 8; ++e) {
+          const float u = x[c * 8 + e];
+          const float au = fabsf(u);
+          const bool p2 = au > T2;
+          const float thr = p2 ? T3 : T1;
+          const bool p1 = au > thr;
+          const uint32_t k4 = (p2 ? 6u : 4u) + (p1 ? 1u : 0u);              // (2*p2 + p1) ^ 4
+          const uint32_t sa = (uint32_t)((int32_t)__float_as_uint(u) >> 31);  // -1 if negative
+          const uint32_t code = (k4 ^ sa) & 7u;  // neg ? 3 - k : 4 + k
+          w |= code << (3 * e);
+          gmin = fminf(gmin, fminf(fabsf(au - T2), fabsf(au - thr)));
+          amin = fminf(amin, au);
+        }
+        words[c] = w;
       }
-      words[c] = w;
+      replay |= (gmin < DL) | (amin < DL);
+    } else {
+      const float inv = N > 0.f ? 1.0f / N : 0.f;
+      float gmin = INFINITY;
+#pragma unroll
+      for (int c = 0; c < G::NCH; ++c) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float z = x[c * 8 + e] * inv;
+          // binary search over the 7 thresholds; both boundaries of the final
+          // cell are on the search path, so the guard checks only those three.
+          const bool p1 = z > m[3];
+          const float t2 = p1 ? m[5] : m[1];
+          const bool p2 = z > t2;
+          const float t3 = p1 ? (p2 ? m[6] : m[4]) : (p2 ? m[2] : m[0]);
+          const bool p3 = z > t3;
+          gmin = fminf(gmin, fminf(fabsf(z - m[3]), fminf(fabsf(z - t2), fabsf(z - t3))));
+          w |= ((p1 ? 4u : 0u) | (p2 ? 2u : 0u) | (p3 ? 1u : 0u)) << (3 * e);
+        }
+        words[c] = w;
+      }
+      replay |= gmin < delta;
     }
     if (zero || nonfinite) {
 #pragma unroll
       for (int c = 0; c < G::NCH; ++c) words[c] = 0;
       scale = 0.f;
     }
-    // all lanes of a vector agree on replay/nonfinite
+    // all lanes of a vector agree on replay
 #pragma unroll
-    for (int lb = 0; lb < G::LB; ++lb) {
-      replay |= __shfl_xor_sync(0xffffffffu, (int)replay, 1 << lb) != 0;
-    }
+    for (int lb = 0; lb < G::LB; ++lb) replay |= __shfl_xor_sync(0xffffffffu, (int)replay, 1 << lb) != 0;
     replay = replay && valid && !nonfinite && !zero;
     if (valid && nonfinite && s == 0) atomicOr(&a.status[layer], PKV_FLAG_V_NONFINITE);
 
@@ -522,89 +584,68 @@ __device__ void v_encode_item(const EncodeArgs& a, int layer, int item, VSmem<D>
     while (mask) {
       const int src_lane = __ffs(mask) - 1;
       mask &= mask - 1;
-      const long long rv = vbase + (long long)it * G::VPI + warp * G::VPW + src_lane / G::TPV;
-      v_replay<D, TIn>(a, layer, rv, sm.R, sm.C);
+      v_replay<D, TIn>(a, layer, vbase + (long long)it * G::VPW + src_lane / G::TPV, sm.R, sm.C);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// persistent encode kernel with ticketed work items
+// encode kernel: static warp schedule over rounds
 // ---------------------------------------------------------------------------
-// Items are ordered in rounds r = 0..L: round r holds the absmax items of
-// layer r, the value items of layer r and the key-encode items of layer r-1
-// (interleaved). A key-encode item waits for its layer's absmax to be
-// complete; all those items hold smaller tickets and never wait, so the
-// schedule is deadlock-free, and layer r-1's keys are re-read from L2.
+// Round r holds the absmax items of layer r, then the value items of layer r
+// interleaved with the key-encode items of layer r - lag. Warp w processes
+// items w, w + W, w + 2W, ... in order. A key-encode item waits for its
+// layer's absmax; all of those carry smaller item indices and never wait, and
+// every warp is co-resident (cooperative launch), so progress is guaranteed.
 struct ItemRef {
   int kind;  // 0 absmax, 1 key encode, 2 value encode
   int layer;
   int idx;
 };
 
-__device__ __forceinline__ ItemRef decode_ticket(const EncodeArgs& a, long long t) {
-  const long long nA = a.a_items, nE = a.e_items, nV = a.v_items;
+__device__ __forceinline__ ItemRef decode_item(const EncodeArgs& a, long long t, int& r) {
+  while (r + 1 < a.num_rounds && t >= a.round_start[r + 1]) ++r;
+  long long off = t - a.round_start[r];
   const int L = a.num_layers;
-  const long long s0 = nA + nV, sm = nA + nV + nE;
-  int r;
-  long long off;
-  if (t < s0) {
-    r = 0;
-    off = t;
-  } else {
-    long long tt = t - s0;
-    if (L > 1 && tt < (long long)(L - 1) * sm) {
-      r = 1 + (int)(tt / sm);
-      off = tt % sm;
-    } else {
-      r = L;
-      off = tt - (long long)(L - 1) * sm;
-    }
-  }
   ItemRef it;
-  if (r < L) {
-    if (off < nA) {
-      it.kind = 0; it.layer = r; it.idx = (int)off;
-      return it;
-    }
-    off -= nA;
-    const long long nE_r = (r >= 1) ? nE : 0;
-    // interleave value items of layer r with key-encode items of layer r-1
-    const long long both = 2 * min(nV, nE_r);
-    if (off < both) {
-      if ((off & 1) == 0) { it.kind = 2; it.layer = r; it.idx = (int)(off >> 1); }
-      else { it.kind = 1; it.layer = r - 1; it.idx = (int)(off >> 1); }
-      return it;
-    }
-    off -= both;
-    if (nV > nE_r) { it.kind = 2; it.layer = r; it.idx = (int)(min(nV, nE_r) + off); }
-    else { it.kind = 1; it.layer = r - 1; it.idx = (int)(min(nV, nE_r) + off); }
+  const long long nA = (r < L) ? a.a_items : 0;
+  const long long nV = (r < L) ? a.v_items : 0;
+  const long long nE = (r >= a.lag && r - a.lag < L) ? a.e_items : 0;
+  if (off < nA) {
+    it.kind = 0; it.layer = r; it.idx = (int)off;
     return it;
   }
-  it.kind = 1; it.layer = L - 1; it.idx = (int)off;
+  off -= nA;
+  const long long both = 2 * min(nV, nE);
+  if (off < both) {
+    if ((off & 1) == 0) { it.kind = 2; it.layer = r; it.idx = (int)(off >> 1); }
+    else { it.kind = 1; it.layer = r - a.lag; it.idx = (int)(off >> 1); }
+    return it;
+  }
+  off -= both;
+  if (nV > nE) { it.kind = 2; it.layer = r; }
+  else { it.kind = 1; it.layer = r - a.lag; }
+  it.idx = (int)(min(nV, nE) + off);
   return it;
 }
 
-template <int D, typename TIn>
+template <int D, typename TIn, bool SYM, bool SIGN>
 __global__ void __launch_bounds__(kThreads, 2) encode_kernel(const __grid_constant__ EncodeArgs a) {
-  __shared__ VSmem<D> vsm[kThreads / 32];
-  __shared__ uint32_t red[kThreads / 32 + 2];
-  __shared__ long long ticket_sh;
-  for (;;) {
-    if (threadIdx.x == 0) ticket_sh = (long long)atomicAdd(a.ws, 1u);
-    __syncthreads();
-    const long long t = ticket_sh;
-    __syncthreads();
-    if (t >= a.total_items) break;
-    const ItemRef it = decode_ticket(a, t);
+  __shared__ VSmem<D> vsm[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  const long long nw = (long long)gridDim.x * kWarps;
+  const unsigned long long smask = SIGN ? lane_sign_mask<D>(a.sign_bits, lane % VG<D>::TPV) : 0ull;
+  int r = 0;
+  for (long long t = gw; t < a.total_items; t += nw) {
+    const ItemRef it = decode_item(a, t, r);
     if (it.kind == 0) {
-      k_absmax_item<TIn>(a, it.layer, it.idx, red);
+      k_absmax_item<TIn>(a, it.layer, it.idx, lane);
     } else if (it.kind == 1) {
-      k_encode_item<TIn>(a, it.layer, it.idx, red);
+      k_encode_item<TIn>(a, it.layer, it.idx, lane);
     } else {
-      v_encode_item<D, TIn>(a, it.layer, it.idx, vsm);
+      v_encode_item<D, TIn, SYM, SIGN>(a, it.layer, it.idx, warp, lane, vsm[warp], smask);
     }
-    __syncthreads();
   }
 }
 
@@ -613,13 +654,12 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(const __grid_consta
 // ---------------------------------------------------------------------------
 
 // int8 code -> exact f32 via the 2^23 magic (no I2F on the conversion pipe)
-__device__ __forceinline__ float i8_to_f32(uint32_t word, int byte) {
-  uint32_t b = (word >> (8 * byte)) & 0xffu;
-  return __uint_as_float(0x4B000000u | (b ^ 0x80u)) - 8388736.0f;
+__device__ __forceinline__ float i8_to_f32(uint32_t word_x80, int byte) {
+  return __uint_as_float(__byte_perm(word_x80, 0x4B000000u, 0x7650 + byte)) - 8388736.0f;
 }
 
 template <typename TOut>
-__device__ void k_decode_item(const DecodeArgs& a, int layer, int item) {
+__device__ void k_decode_item(const DecodeArgs& a, int layer, int item, int lane) {
   const int8_t* codes = a.k_codes[layer];
   TOut* out = static_cast<TOut*>(a.k_out[layer]);
   const long long e0 = (long long)item * kKElems;
@@ -627,22 +667,23 @@ __device__ void k_decode_item(const DecodeArgs& a, int layer, int item) {
   const bool tensor = a.k_mode == PKV_K_TENSOR;
   const float ts = tensor ? __ldg(a.k_scale[layer]) : 0.f;
   if (a.vec_ok) {
-#pragma unroll
-    for (int i = 0; i < kKElems / (kThreads * 8); ++i) {
-      long long e = e0 + ((long long)i * kThreads + threadIdx.x) * 8;
+#pragma unroll 4
+    for (int i = 0; i < kKChunks; ++i) {
+      const long long e = e0 + ((long long)i * 32 + lane) * 8;
       if (e >= n) continue;
       const uint2 w = ld_stream_u2(codes + e);
       const float s = tensor ? ts : __half2float(__ldg(a.k_bscale[layer] + (e >> 5)));
+      const uint32_t wx = w.x ^ 0x80808080u, wy = w.y ^ 0x80808080u;
       float y[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) y[j] = i8_to_f32(w.x, j) * s;
+      for (int j = 0; j < 4; ++j) y[j] = i8_to_f32(wx, j) * s;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) y[4 + j] = i8_to_f32(w.y, j) * s;
+      for (int j = 0; j < 4; ++j) y[4 + j] = i8_to_f32(wy, j) * s;
       store8(out + e, y);
     }
   } else {
-    for (int i = threadIdx.x; i < kKElems; i += kThreads) {
-      long long e = e0 + i;
+    for (int i = lane; i < kKElems; i += 32) {
+      const long long e = e0 + i;
       if (e >= n) continue;
       const float s = tensor ? ts : __half2float(__ldg(a.k_bscale[layer] + (e >> 5)));
       store1(out + e, (float)codes[e] * s);
@@ -650,51 +691,44 @@ __device__ void k_decode_item(const DecodeArgs& a, int layer, int item) {
   }
 }
 
-template <int D, typename TOut>
-__device__ void v_decode_item(const DecodeArgs& a, int layer, int item, uint32_t* stage_all,
-                              float* tbl) {
+// x / f32(sqrt(D)), correctly rounded. Power-of-four D: exact multiply.
+// Otherwise q = x*r corrected once with the exact FMA remainder; the
+// sequence is verified exhaustively over all f32 mantissas by
+// pkv_selftest(PKV_SELFTEST_DIVISION) and falls back to IEEE division
+// outside the normal range.
+template <int D>
+__device__ __forceinline__ float div_sqrt_d(float x, float c, float r) {
+  constexpr bool pow4 = (VG<D>::LOG2D % 2) == 0;
+  if (pow4) return x * r;
+  const float q = x * r;
+  const float e = fmaf(-q, c, x);
+  const float q1 = fmaf(e, r, q);
+  // the correction turns -0 / c into +0; the quotient has the sign of x
+  return __uint_as_float((__float_as_uint(q1) & 0x7fffffffu) | (__float_as_uint(x) & 0x80000000u));
+}
+
+template <int D, typename TOut, bool SIGN>
+__device__ void v_decode_item(const DecodeArgs& a, int layer, int item, int warp, int lane,
+                              uint32_t (*stage)[VG<D>::W + 1], float* tbl, unsigned long long smask) {
   using G = VG<D>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int vw = lane / G::TPV, s = lane % G::TPV;
-  uint32_t(*stage)[G::W + 1] =
-      reinterpret_cast<uint32_t(*)[G::W + 1]>(stage_all + warp * G::VPW * (G::W + 1));
   const uint8_t* packed = a.v_packed[layer];
   const float* scales = a.v_scales[layer];
   TOut* out = static_cast<TOut*>(a.v_out[layer]);
   const long long vbase = (long long)item * VItem<D>::VECS;
-  const float sqd = a.sqrt_d32;
+  const float sqd = a.sqrt_d32, rsqd = a.rcp_sqrt_d32;
+  const uint32_t lane_off = (uint32_t)threadIdx.x * 4u;  // byte offset of this lane's table column
+  char* tbl_base = reinterpret_cast<char*>(tbl);
 
+#pragma unroll 1
   for (int itr = 0; itr < VItem<D>::ITERS; ++itr) {
-    const long long v = vbase + (long long)itr * G::VPI + warp * G::VPW + vw;
+    const long long v = vbase + (long long)itr * G::VPW + vw;
     const bool valid = v < a.nvec;
     // each lane fetches its Q contiguous packed words, then a warp transpose
     // hands every lane the words of its own chunks
     uint32_t q[G::Q];
     if (valid) {
-      const uint8_t* p = packed + v * G::PACKED_BYTES + s * 3 * G::Q;
-      if constexpr (G::Q == 8) {
-        const uint2 u0 = ld_stream_u2(p), u1 = ld_stream_u2(p + 8), u2 = ld_stream_u2(p + 16);
-        const uint32_t u[6] = {u0.x, u0.y, u1.x, u1.y, u2.x, u2.y};
-        q[0] = u[0] & 0xffffffu;
-        q[1] = ((u[0] >> 24) | (u[1] << 8)) & 0xffffffu;
-        q[2] = ((u[1] >> 16) | (u[2] << 16)) & 0xffffffu;
-        q[3] = u[2] >> 8;
-        q[4] = u[3] & 0xffffffu;
-        q[5] = ((u[3] >> 24) | (u[4] << 8)) & 0xffffffu;
-        q[6] = ((u[4] >> 16) | (u[5] << 16)) & 0xffffffu;
-        q[7] = u[5] >> 8;
-      } else if constexpr (G::Q == 4) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
-        const uint32_t u0 = __ldg(w), u1 = __ldg(w + 1), u2 = __ldg(w + 2);
-        q[0] = u0 & 0xffffffu;
-        q[1] = ((u0 >> 24) | (u1 << 8)) & 0xffffffu;
-        q[2] = ((u1 >> 16) | (u2 << 16)) & 0xffffffu;
-        q[3] = u2 >> 8;
-      } else {
-#pragma unroll
-        for (int j = 0; j < G::Q; ++j)
-          q[j] = (uint32_t)p[3 * j] | ((uint32_t)p[3 * j + 1] << 8) | ((uint32_t)p[3 * j + 2] << 16);
-      }
+      load_words<G::Q>(packed + v * G::PACKED_BYTES + s * 3 * G::Q, q);
     } else {
 #pragma unroll
       for (int j = 0; j < G::Q; ++j) q[j] = 0;
@@ -716,19 +750,27 @@ __device__ void v_decode_item(const DecodeArgs& a, int layer, int item, uint32_t
 #pragma unroll
     for (int c = 0; c < G::NCH; ++c)
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        x[c * 8 + e] = tbl[((words[c] >> (3 * e)) & 7u) * kThreads + threadIdx.x];
+      for (int e = 0; e < 8; ++e) {
+        // byte address (code << 10) | lane_off  (kThreads * 4 == 1024)
+        const uint32_t sh = 3 * e;
+        const uint32_t off = (sh <= 10 ? (words[c] << (10 - sh)) : (words[c] >> (sh - 10))) & 0x1c00u;
+        x[c * 8 + e] = *reinterpret_cast<const float*>(tbl_base + (off | lane_off));
+      }
 
     fwht_lanes<D>(x, s);
 
+    if (sc >= 0x1p-80f || sc == 0.f) {
 #pragma unroll
-    for (int i = 0; i < G::CPT; ++i) x[i] = x[i] / sqd;  // IEEE division (fwht.py:50)
-    if (a.use_sign) {
+      for (int i = 0; i < G::CPT; ++i) x[i] = div_sqrt_d<D>(x[i], sqd, rsqd);  // fwht.py:50
+    } else {
+      // tiny scales can produce subnormal quotients: plain IEEE division
 #pragma unroll
-      for (int c = 0; c < G::NCH; ++c)
+      for (int i = 0; i < G::CPT; ++i) x[i] = __fdiv_rn(x[i], sqd);
+    }
+    if (SIGN) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (sign_bit(a.sign_bits, 8 * (s + G::TPV * c) + e)) x[c * 8 + e] = -x[c * 8 + e];
+      for (int i = 0; i < G::CPT; ++i)
+        x[i] = __uint_as_float(__float_as_uint(x[i]) ^ ((uint32_t)(smask >> i) << 31));
     }
     if (valid) {
       TOut* o = out + v * D;
@@ -740,30 +782,36 @@ __device__ void v_decode_item(const DecodeArgs& a, int layer, int item, uint32_t
         store8(o + 8 * (s + G::TPV * c), y);
       }
     }
+    __syncwarp();
   }
 }
 
-template <int D, typename TOut>
+template <int D, typename TOut, bool SIGN>
 __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_constant__ DecodeArgs a) {
-  __shared__ uint32_t stage[kThreads / VG<D>::TPV * (VG<D>::W + 1)];
+  using G = VG<D>;
+  __shared__ uint32_t stage[kWarps][G::VPW][G::W + 1];
   __shared__ float tbl[8 * kThreads];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * kWarps + warp;
+  const long long nw = (long long)gridDim.x * kWarps;
+  const unsigned long long smask = SIGN ? lane_sign_mask<D>(a.sign_bits, lane % G::TPV) : 0ull;
   const long long per_layer = (long long)a.k_items + a.v_items;
-  for (long long t = blockIdx.x; t < a.total_items; t += gridDim.x) {
+  const long long both = 2 * (long long)min(a.k_items, a.v_items);
+  for (long long t = gw; t < a.total_items; t += nw) {
     const int layer = (int)(t / per_layer);
-    long long off = t % per_layer;
+    long long off = t - (long long)layer * per_layer;
     // interleave key and value items so memory- and ALU-heavy work overlap
-    const long long both = 2 * (long long)min(a.k_items, a.v_items);
     int kind, idx;
     if (off < both) {
-      kind = (off & 1) ? 1 : 0;
+      kind = (int)(off & 1);
       idx = (int)(off >> 1);
     } else {
       off -= both;
       kind = a.k_items > a.v_items ? 0 : 1;
       idx = (int)(min(a.k_items, a.v_items) + off);
     }
-    if (kind == 0) k_decode_item<TOut>(a, layer, idx);
-    else v_decode_item<D, TOut>(a, layer, idx, stage, tbl);
+    if (kind == 0) k_decode_item<TOut>(a, layer, idx, lane);
+    else v_decode_item<D, TOut, SIGN>(a, layer, idx, warp, lane, stage[warp], tbl, smask);
   }
 }
 
@@ -775,10 +823,10 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ packed, long long coun
   const long long groups = (count + 7) / 8;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
        g += (long long)gridDim.x * blockDim.x) {
-    uint32_t w = (uint32_t)packed[3 * g] | ((uint32_t)packed[3 * g + 1] << 8) |
-                 ((uint32_t)packed[3 * g + 2] << 16);
+    const uint32_t w = (uint32_t)packed[3 * g] | ((uint32_t)packed[3 * g + 1] << 8) |
+                       ((uint32_t)packed[3 * g + 2] << 16);
     for (int e = 0; e < 8; ++e) {
-      long long i = 8 * g + e;
+      const long long i = 8 * g + e;
       if (i < count) codes[i] = (uint8_t)((w >> (3 * e)) & 7u);
     }
   }
@@ -792,8 +840,8 @@ __global__ void pack_kernel(const uint8_t* __restrict__ codes, long long count,
     uint32_t w = 0;
     bool oob = false;
     for (int e = 0; e < 8; ++e) {
-      long long i = 8 * g + e;
-      uint32_t c = i < count ? codes[i] : 0u;
+      const long long i = 8 * g + e;
+      const uint32_t c = i < count ? codes[i] : 0u;
       oob |= c > 7u;
       w |= (c & 7u) << (3 * e);
     }
@@ -802,6 +850,21 @@ __global__ void pack_kernel(const uint8_t* __restrict__ codes, long long count,
     packed[3 * g + 1] = (uint8_t)((w >> 8) & 0xff);
     packed[3 * g + 2] = (uint8_t)((w >> 16) & 0xff);
   }
+}
+
+// Exhaustive check of div_sqrt_d<D> against IEEE division for every f32
+// mantissa in [1, 2) (exponent scaling is exact in the normal range).
+template <int D>
+__global__ void selftest_div_kernel(uint32_t* mismatches) {
+  const float c = (float)sqrt((double)D);
+  const float r = 1.0f / c;
+  uint32_t bad = 0;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < (1u << 23); m += gridDim.x * blockDim.x) {
+    const float x = __uint_as_float(0x3f800000u | m);
+    bad += __float_as_uint(div_sqrt_d<D>(x, c, r)) != __float_as_uint(__fdiv_rn(x, c));
+    bad += __float_as_uint(div_sqrt_d<D>(-x * 0x1p-60f, c, r)) != __float_as_uint(__fdiv_rn(-x * 0x1p-60f, c));
+  }
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 }  // namespace pkv
@@ -820,10 +883,10 @@ bool pinned_midpoints(const double* c, double* mid) {
     if (!(c[i + 1] > c[i])) return false;
     // largest double not above the exact rational midpoint
     // (valuequant.py:62-71): TwoSum gives the exact a+b = s + e.
-    const double a = c[i], b = c[i + 1];
-    const double s = a + b;
-    const double bb = s - a;
-    const double e = (a - (s - bb)) + (b - bb);
+    const double x = c[i], y = c[i + 1];
+    const double s = x + y;
+    const double bb = s - x;
+    const double e = (x - (s - bb)) + (y - bb);
     double m = s * 0.5;
     if (e < 0.0) m = std::nextafter(m, -INFINITY);
     mid[i] = m;
@@ -836,6 +899,9 @@ bool fill_codebook(const double* centroids, Codebook3& cb) {
   if (!pinned_midpoints(centroids, cb.mid64)) return false;
   for (int i = 0; i < 7; ++i) cb.mid32[i] = (float)cb.mid64[i];
   for (int i = 0; i < 8; ++i) cb.cent32[i] = (float)centroids[i];
+  bool sym = true;
+  for (int i = 0; i < 8; ++i) sym = sym && centroids[i] == -centroids[7 - i];
+  cb.symmetric = sym ? 1 : 0;
   return true;
 }
 
@@ -852,72 +918,93 @@ float guard_delta(int d) {
   return (float)(1.5 * u * (log2i(d) * std::sqrt((double)d) + 6.0) + 1e-12);
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
-int occupancy_grid(const void* fn, int smem) {
-  int dev = 0, sms = 148, per_sm = 1;
+int sm_count() {
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess ||
-      per_sm < 1)
+  return sms;
+}
+
+int blocks_per_sm(const void* fn) {
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1)
     per_sm = 1;
-  return sms * per_sm;
+  return per_sm;
+}
+
+template <int D, typename TIn, bool SYM, bool SIGN>
+int launch_encode(EncodeArgs& a, cudaStream_t st) {
+  auto fn = encode_kernel<D, TIn, SYM, SIGN>;
+  const int per_sm = blocks_per_sm((const void*)fn);
+  long long grid = (long long)sm_count() * per_sm;
+  const long long need = (a.total_items + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
+  if (grid < 1) return PKV_OK;
+  void* params[] = {(void*)&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)grid), dim3(kThreads),
+                                                    params, 0, st);
+  return e == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D, typename TIn>
-int launch_encode(EncodeArgs& a, cudaStream_t st) {
-  const void* fn = (const void*)encode_kernel<D, TIn>;
-  int grid = occupancy_grid(fn, 0);
-  if ((long long)grid > a.total_items) grid = (int)a.total_items;
-  if (grid < 1) return PKV_OK;
-  encode_kernel<D, TIn><<<grid, kThreads, 0, st>>>(a);
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+int launch_encode_d(EncodeArgs& a, cudaStream_t st, bool sym, bool sign) {
+  if (sym) return sign ? launch_encode<D, TIn, true, true>(a, st) : launch_encode<D, TIn, true, false>(a, st);
+  return sign ? launch_encode<D, TIn, false, true>(a, st) : launch_encode<D, TIn, false, false>(a, st);
 }
 
 template <typename TIn>
-int dispatch_encode(EncodeArgs& a, cudaStream_t st) {
-  switch (a.do_v ? a.head_dim : 128) {
-    case 8: return launch_encode<8, TIn>(a, st);
-    case 16: return launch_encode<16, TIn>(a, st);
-    case 32: return launch_encode<32, TIn>(a, st);
-    case 64: return launch_encode<64, TIn>(a, st);
-    case 128: return launch_encode<128, TIn>(a, st);
-    case 256: return launch_encode<256, TIn>(a, st);
+int dispatch_encode(EncodeArgs& a, cudaStream_t st, bool do_v, bool sym, bool sign) {
+  switch (do_v ? a.head_dim : 128) {
+    case 8: return launch_encode_d<8, TIn>(a, st, sym, sign);
+    case 16: return launch_encode_d<16, TIn>(a, st, sym, sign);
+    case 32: return launch_encode_d<32, TIn>(a, st, sym, sign);
+    case 64: return launch_encode_d<64, TIn>(a, st, sym, sign);
+    case 128: return launch_encode_d<128, TIn>(a, st, sym, sign);
+    case 256: return launch_encode_d<256, TIn>(a, st, sym, sign);
     default: return PKV_ERR_UNSUPPORTED_HEAD_DIM;
   }
 }
 
-template <int D, typename TOut>
+template <int D, typename TOut, bool SIGN>
 int launch_decode(DecodeArgs& a, cudaStream_t st) {
-  const void* fn = (const void*)decode_kernel<D, TOut>;
-  long long grid = occupancy_grid(fn, 0);
-  if (grid > a.total_items) grid = a.total_items;
+  auto fn = decode_kernel<D, TOut, SIGN>;
+  long long grid = (long long)sm_count() * blocks_per_sm((const void*)fn);
+  const long long need = (a.total_items + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
   if (grid < 1) return PKV_OK;
-  decode_kernel<D, TOut><<<(int)grid, kThreads, 0, st>>>(a);
+  fn<<<(unsigned)grid, kThreads, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
 
+template <int D, typename TOut>
+int launch_decode_d(DecodeArgs& a, cudaStream_t st, bool sign) {
+  return sign ? launch_decode<D, TOut, true>(a, st) : launch_decode<D, TOut, false>(a, st);
+}
+
 template <typename TOut>
-int dispatch_decode(DecodeArgs& a, cudaStream_t st) {
-  switch (a.do_v ? a.head_dim : 128) {
-    case 8: return launch_decode<8, TOut>(a, st);
-    case 16: return launch_decode<16, TOut>(a, st);
-    case 32: return launch_decode<32, TOut>(a, st);
-    case 64: return launch_decode<64, TOut>(a, st);
-    case 128: return launch_decode<128, TOut>(a, st);
-    case 256: return launch_decode<256, TOut>(a, st);
+int dispatch_decode(DecodeArgs& a, cudaStream_t st, bool do_v, bool sign) {
+  switch (do_v ? a.head_dim : 128) {
+    case 8: return launch_decode_d<8, TOut>(a, st, sign);
+    case 16: return launch_decode_d<16, TOut>(a, st, sign);
+    case 32: return launch_decode_d<32, TOut>(a, st, sign);
+    case 64: return launch_decode_d<64, TOut>(a, st, sign);
+    case 128: return launch_decode_d<128, TOut>(a, st, sign);
+    case 256: return launch_decode_d<256, TOut>(a, st, sign);
     default: return PKV_ERR_UNSUPPORTED_HEAD_DIM;
   }
 }
 
-void fill_sign(const uint32_t* sign_bits_host, int d, uint32_t* dst, int* use) {
+bool fill_sign(const uint32_t* sign_bits_host, int d, uint32_t* dst) {
   std::memset(dst, 0, 8 * sizeof(uint32_t));
-  *use = 0;
-  if (!sign_bits_host) return;
+  if (!sign_bits_host) return false;
   const int words = (d + 31) / 32;
+  bool any = false;
   for (int i = 0; i < words && i < 8; ++i) dst[i] = sign_bits_host[i];
   if (d % 32) dst[words - 1] &= (1u << (d % 32)) - 1u;
-  *use = 1;
+  for (int i = 0; i < 8; ++i) any = any || dst[i] != 0;
+  return any;
 }
 
 template <int D>
@@ -935,6 +1022,12 @@ int v_items_dispatch(int d, long long nvec) {
     case 256: return v_items_for<256>(nvec);
     default: return -1;
   }
+}
+
+// alignment the value kernels need for the packed stream of head_dim d
+uintptr_t packed_align(int d) {
+  const int q = (d / 8) / (d >= 256 ? 4 : (d >= 16 ? 2 : 1));
+  return q >= 8 ? 8 : (q >= 4 ? 4 : (q >= 2 ? 2 : 1));
 }
 
 }  // namespace
@@ -963,7 +1056,7 @@ int pkv_v_head_dim_supported(int d) {
 size_t pkv_encode_workspace_bytes(int num_layers) {
   if (num_layers < 0) return 0;
   const int l = std::min(num_layers, (int)PKV_MAX_LAYERS_PER_LAUNCH);
-  return (size_t)(1 + 2 * l) * sizeof(uint32_t);
+  return (size_t)(2 * l + 2) * sizeof(uint32_t);
 }
 
 int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
@@ -981,7 +1074,6 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
   if (do_v && !pkv_v_head_dim_supported(head_dim)) return PKV_ERR_UNSUPPORTED_HEAD_DIM;
   if (workspace_bytes < pkv_encode_workspace_bytes(num_layers) || !workspace) return PKV_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int elt = in_dtype == PKV_F32 ? 4 : 2;
   const long long nelem = (long long)num_vectors * head_dim;
 
   for (int l0 = 0; l0 < num_layers; l0 += PKV_MAX_LAYERS_PER_LAUNCH) {
@@ -991,12 +1083,10 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     a.num_layers = L;
     a.head_dim = head_dim;
     a.k_mode = k_mode;
-    a.do_k = do_k;
-    a.do_v = do_v;
     a.nvec = num_vectors;
     a.nelem = nelem;
     a.delta = guard_delta(head_dim);
-    fill_sign(sign_bits_host, head_dim, a.sign_bits, &a.use_sign);
+    const bool sign = fill_sign(sign_bits_host, head_dim, a.sign_bits);
     if (do_v && !fill_codebook(centroids_host, a.cb)) return PKV_ERR_UNSUPPORTED_CODEBOOK;
     a.status = status + l0;
     a.replay_count = replay_count;
@@ -1014,7 +1104,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
           a.k_bscale[l] = k_bscale ? reinterpret_cast<__half*>(k_bscale[l0 + l]) : nullptr;
           if (!a.k_bscale[l]) return PKV_ERR_INVALID_ARG;
         }
-        ok = ok && aligned16(a.k_in[l]) && (reinterpret_cast<uintptr_t>(a.k_codes[l]) & 7u) == 0;
+        ok = ok && aligned(a.k_in[l], 16) && aligned(a.k_codes[l], 8);
       }
       if (do_v) {
         a.v_in[l] = v_in[l0 + l];
@@ -1022,22 +1112,37 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
         a.v_scales[l] = v_scales ? v_scales[l0 + l] : nullptr;
         if (!a.v_in[l] || !a.v_packed[l] || !a.v_scales[l]) return PKV_ERR_INVALID_ARG;
         // the value kernels use 16 B chunk loads and word-aligned packed stores
-        if (!aligned16(a.v_in[l]) || (reinterpret_cast<uintptr_t>(a.v_packed[l]) & 7u) ||
-            (reinterpret_cast<uintptr_t>(a.v_scales[l]) & 3u))
+        if (!aligned(a.v_in[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim)) ||
+            !aligned(a.v_scales[l], 4))
           return PKV_ERR_ALIGNMENT;
       }
     }
-    (void)elt;
     a.vec_ok = ok ? 1 : 0;
     const int k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;
     a.e_items = k_items;
     a.a_items = (do_k && k_mode == PKV_K_TENSOR) ? k_items : 0;
     a.v_items = do_v ? v_items_dispatch(head_dim, num_vectors) : 0;
-    a.total_items = (long long)L * (a.a_items + a.e_items + a.v_items);
-    if (cudaMemsetAsync(workspace, 0, pkv_encode_workspace_bytes(L), st) != cudaSuccess)
-      return PKV_ERR_CUDA;
-    const int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st)
-                                       : dispatch_encode<__nv_bfloat16>(a, st);
+    // lag: keep >= ~2 waves of warps between a layer's absmax and its key encode
+    const long long round = (long long)a.a_items + a.v_items + a.e_items;
+    const long long warps = (long long)sm_count() * 2 * kWarps;
+    int lag = 1;
+    if (a.a_items > 0) {
+      while (lag < 8 && (long long)lag * round < 2 * warps) ++lag;
+    }
+    a.lag = lag;
+    a.num_rounds = L + lag;
+    long long acc = 0;
+    for (int r = 0; r < a.num_rounds; ++r) {
+      a.round_start[r] = acc;
+      if (r < L) acc += a.a_items + a.v_items;
+      if (r >= lag && r - lag < L) acc += a.e_items;
+    }
+    a.round_start[a.num_rounds] = acc;
+    a.total_items = acc;
+    if (cudaMemsetAsync(workspace, 0, pkv_encode_workspace_bytes(L), st) != cudaSuccess) return PKV_ERR_CUDA;
+    const bool sym = do_v ? a.cb.symmetric != 0 : true;
+    const int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st, do_v, sym, sign)
+                                       : dispatch_encode<__nv_bfloat16>(a, st, do_v, sym, sign);
     if (rc != PKV_OK) return rc;
   }
   return PKV_OK;
@@ -1065,12 +1170,11 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
     a.num_layers = L;
     a.head_dim = head_dim;
     a.k_mode = k_mode;
-    a.do_k = do_k;
-    a.do_v = do_v;
     a.nvec = num_vectors;
     a.nelem = nelem;
     a.sqrt_d32 = (float)std::sqrt((double)head_dim);  // np.float32(np.sqrt(d))
-    fill_sign(sign_bits_host, head_dim, a.sign_bits, &a.use_sign);
+    a.rcp_sqrt_d32 = 1.0f / a.sqrt_d32;
+    const bool sign = fill_sign(sign_bits_host, head_dim, a.sign_bits);
     if (do_v) {
       Codebook3 cb;
       if (!fill_codebook(centroids_host, cb)) return PKV_ERR_UNSUPPORTED_CODEBOOK;
@@ -1083,26 +1187,24 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
         a.k_out[l] = k_out[l0 + l];
         if (k_mode == PKV_K_TENSOR) a.k_scale[l] = k_scale ? k_scale[l0 + l] : nullptr;
         else a.k_bscale[l] = k_bscale ? reinterpret_cast<const __half*>(k_bscale[l0 + l]) : nullptr;
-        if (!a.k_codes[l] || !a.k_out[l] ||
-            (k_mode == PKV_K_TENSOR ? !a.k_scale[l] : !a.k_bscale[l]))
+        if (!a.k_codes[l] || !a.k_out[l] || (k_mode == PKV_K_TENSOR ? !a.k_scale[l] : !a.k_bscale[l]))
           return PKV_ERR_INVALID_ARG;
-        ok = ok && (reinterpret_cast<uintptr_t>(a.k_codes[l]) & 7u) == 0 && aligned16(a.k_out[l]);
+        ok = ok && aligned(a.k_codes[l], 8) && aligned(a.k_out[l], 16);
       }
       if (do_v) {
         a.v_packed[l] = v_packed[l0 + l];
         a.v_scales[l] = v_scales ? v_scales[l0 + l] : nullptr;
         a.v_out[l] = v_out[l0 + l];
         if (!a.v_packed[l] || !a.v_scales[l] || !a.v_out[l]) return PKV_ERR_INVALID_ARG;
-        if (!aligned16(a.v_out[l]) || (reinterpret_cast<uintptr_t>(a.v_packed[l]) & 7u))
-          return PKV_ERR_ALIGNMENT;
+        if (!aligned(a.v_out[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim))) return PKV_ERR_ALIGNMENT;
       }
     }
     a.vec_ok = ok ? 1 : 0;
     a.k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;
     a.v_items = do_v ? v_items_dispatch(head_dim, num_vectors) : 0;
     a.total_items = (long long)L * (a.k_items + a.v_items);
-    const int rc = out_dtype == PKV_F32 ? dispatch_decode<float>(a, st)
-                                        : dispatch_decode<__nv_bfloat16>(a, st);
+    const int rc = out_dtype == PKV_F32 ? dispatch_decode<float>(a, st, do_v, sign)
+                                        : dispatch_decode<__nv_bfloat16>(a, st, do_v, sign);
     if (rc != PKV_OK) return rc;
   }
   return PKV_OK;
@@ -1112,7 +1214,7 @@ int pkv_unpack_codes(const uint8_t* packed, int64_t count, uint8_t* codes, void*
   if (count < 0 || (count > 0 && (!packed || !codes))) return PKV_ERR_INVALID_ARG;
   if (count == 0) return PKV_OK;
   const long long groups = (count + 7) / 8;
-  int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
+  const int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
   unpack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(packed, count, codes);
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
@@ -1122,9 +1224,24 @@ int pkv_pack_codes(const uint8_t* codes, int64_t count, uint8_t* packed, uint32_
   if (count < 0 || (count > 0 && (!packed || !codes))) return PKV_ERR_INVALID_ARG;
   if (count == 0) return PKV_OK;
   const long long groups = (count + 7) / 8;
-  int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
+  const int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
   pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(codes, count, packed, bad_code);
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+}
+
+int64_t pkv_selftest(int what, void* scratch, size_t scratch_bytes, void* stream) {
+  if (what != PKV_SELFTEST_DIVISION) return PKV_ERR_INVALID_ARG;
+  if (!scratch || scratch_bytes < 3 * sizeof(uint32_t)) return PKV_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t* cnt = static_cast<uint32_t*>(scratch);
+  if (cudaMemsetAsync(cnt, 0, 3 * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
+  selftest_div_kernel<8><<<1024, 256, 0, st>>>(cnt + 0);
+  selftest_div_kernel<32><<<1024, 256, 0, st>>>(cnt + 1);
+  selftest_div_kernel<128><<<1024, 256, 0, st>>>(cnt + 2);
+  uint32_t host[3] = {0, 0, 0};
+  if (cudaMemcpyAsync(host, cnt, sizeof(host), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PKV_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PKV_ERR_CUDA;
+  return (int64_t)host[0] + host[1] + host[2];
 }
 
 }  // extern "C"

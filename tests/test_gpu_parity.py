@@ -237,3 +237,12 @@ def test_decode_attention_matches_fp64_oracle():
     got = out.cpu().numpy().astype(np.float64)
     rel = np.abs(got - want).max() / np.abs(want).max()
     assert rel < 1e-3, rel
+
+
+def test_decode_division_sequence_is_correctly_rounded():
+    # exhaustive over all f32 mantissas for d in {8, 32, 128} (pkv_selftest)
+    from paper_2604_24971_b200 import _lib
+
+    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    n = _lib.load().pkv_selftest(1, scratch.data_ptr(), 16, torch.cuda.current_stream().cuda_stream)
+    assert n == 0, f"{n} mismatches vs IEEE division"
