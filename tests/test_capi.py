@@ -48,7 +48,7 @@ def test_abi_and_status(lib):
     assert lib.pkv_status_string(0) == b"ok"
     assert b"head_dim" in lib.pkv_status_string(-2)
     assert lib.pkv_v_head_dim_supported(128) == 1 and lib.pkv_v_head_dim_supported(4) == 0
-    assert lib.pkv_encode_workspace_bytes(32) == (1 + 64) * 4
+    assert lib.pkv_encode_workspace_bytes(32) == (2 * 32 + 2) * 4
 
 
 def test_invalid_arguments_fail_without_touching_the_device(lib):
