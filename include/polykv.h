@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PKV_ABI_VERSION 1
+#define PKV_ABI_VERSION 2
 
 /* status codes */
 #define PKV_OK 0
@@ -70,8 +70,10 @@ const char* pkv_status_string(int status);
  * Key kernels accept any head_dim. Returns 1 if supported. */
 int pkv_v_head_dim_supported(int head_dim);
 
-/* Bytes of device workspace pkv_encode needs for `num_layers` layers. */
-size_t pkv_encode_workspace_bytes(int num_layers);
+/* Bytes of device workspace pkv_encode needs for `num_layers` layers of
+ * `num_vectors` head vectors of `head_dim` (per-layer key maxima are staged
+ * there, one 64-bit word per 16384 key elements). */
+size_t pkv_encode_workspace_bytes(int num_layers, int64_t num_vectors, int head_dim);
 
 /*
  * pkv_encode — write side of the pool for `num_layers` layers in one launch.
@@ -95,7 +97,8 @@ size_t pkv_encode_workspace_bytes(int num_layers);
  *  status            device uint32[num_layers], OR-ed with PKV_FLAG_* bits.
  *  replay_count      device uint32[1] or NULL: incremented once per head vector
  *                    that was re-coded on the exact fp64 path.
- *  workspace         device scratch of pkv_encode_workspace_bytes(num_layers).
+ *  workspace         device scratch of pkv_encode_workspace_bytes(num_layers,
+ *                    num_vectors, head_dim).
  */
 int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
                const void* const* k_in, const void* const* v_in, int k_mode,

@@ -61,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     build_dir = LIB_DIR / "obj"
     build_dir.mkdir(exist_ok=True)
+    procs = []
     for src in sources():
         obj = build_dir / (src.stem + ".o")
         cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
@@ -68,8 +69,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             cmd.insert(1, "-Xptxas=-v" if verbose else "-Xptxas=-O3")
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        procs.append((cmd, subprocess.Popen(cmd)))  # translation units compile in parallel
         objs.append(obj)
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
     tmp = LIB_PATH.with_suffix(".so.tmp")
     link = [nvcc, *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     subprocess.run(link, check=True)

@@ -98,7 +98,7 @@ def encode(
             raise TypeError("all inputs of one encode call must share a dtype")
         if t.device != device or not t.is_contiguous():
             raise ValueError("encode inputs must be contiguous tensors on the pool device")
-    ws_bytes = lib.pkv_encode_workspace_bytes(L)
+    ws_bytes = lib.pkv_encode_workspace_bytes(L, num_vectors, head_dim)
     ws = torch.empty((ws_bytes + 3) // 4, dtype=torch.int32, device=device)
     arr = lambda ts: None if ts is None else ptr_array([_p(t) for t in ts])  # noqa: E731
     rc = lib.pkv_encode(

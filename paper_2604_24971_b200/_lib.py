@@ -39,7 +39,7 @@ SIGNATURES: dict[str, tuple] = {
     "pkv_abi_version": (c_int, []),
     "pkv_status_string": (ctypes.c_char_p, [c_int]),
     "pkv_v_head_dim_supported": (c_int, [c_int]),
-    "pkv_encode_workspace_bytes": (c_size, [c_int]),
+    "pkv_encode_workspace_bytes": (c_size, [c_int, c_i64, c_int]),
     "pkv_encode": (
         c_int,
         [c_int, c_i64, c_int, c_int, P(c_void_p), P(c_void_p), c_int, P(c_void_p), P(c_void_p),

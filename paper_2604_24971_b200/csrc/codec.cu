@@ -27,20 +27,17 @@
 // of layer l wait for layer l's absmax) deadlock-free without atomics on a
 // ticket counter.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
 #include "../../include/polykv.h"
 #include "pkv_common.cuh"
+#include "codec_common.cuh"
+#include "stream_codec.h"
 
 namespace pkv {
 
-struct Codebook3 {
-  float mid32[7];
-  float cent32[8];
-  double mid64[7];
-  int symmetric;
-};
 
 constexpr int kMaxRounds = kMaxLayers + 16;
 
@@ -95,8 +92,6 @@ struct DecodeArgs {
 constexpr int kWarps = kThreads / 32;
 constexpr int kKChunks = 32;                 // 8-element chunks per lane per key item
 constexpr int kKElems = 32 * 8 * kKChunks;   // key elements per warp item (8192)
-constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
-constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
 
 template <int D>
 struct VItem {
@@ -115,47 +110,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // keys
 // ---------------------------------------------------------------------------
 
-// Reference formula (keyquant.py:61-64), evaluated exactly as numpy does in
-// fp64: q = f64(x)/scale, code = floor(|q| + 0.5) * sign(q), clipped.
-__device__ __forceinline__ int key_code_exact(float x, float s, int lo, int hi) {
-  double q = (double)x / (double)s;
-  double r = floor(fabs(q) + 0.5);
-  if (q < 0.0) r = -r;
-  if (r < lo) r = lo;
-  if (r > hi) r = hi;
-  return (int)r;
-}
 
-// 8 key codes of one chunk. Fast path: q = x * (1/s) rounded to nearest via
-// the 2^23 magic; the low byte of the magic sum is the two's-complement code.
-// Elements within kKeyEps of a half-point fall back to the exact formula.
-template <bool CLIP>
-__device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float rcp, bool force_exact) {
-  float m[8];
-  float worst = 0.f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float q = x[j] * rcp;
-    if (CLIP) q = fminf(fmaxf(q, -127.f), 127.f);
-    m[j] = q + kMagic;
-    const float n = m[j] - kMagic;
-    worst = fmaxf(worst, fabsf(q - n));
-  }
-  uint2 w;
-  w.x = __byte_perm(__byte_perm(__float_as_uint(m[0]), __float_as_uint(m[1]), 0x0040),
-                    __byte_perm(__float_as_uint(m[2]), __float_as_uint(m[3]), 0x0040), 0x5410);
-  w.y = __byte_perm(__byte_perm(__float_as_uint(m[4]), __float_as_uint(m[5]), 0x0040),
-                    __byte_perm(__float_as_uint(m[6]), __float_as_uint(m[7]), 0x0040), 0x5410);
-  if (force_exact || worst > 0.5f - kKeyEps) {
-    uint32_t c[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, CLIP ? -127 : -128, 127) & 0xffu);
-    w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-    w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-  }
-  return w;
-}
 
 // |x| bit patterns of 8 inputs, max-reduced without unpacking bf16
 __device__ __forceinline__ uint32_t chunk_absmax_bits(const float* p) {
@@ -653,10 +608,6 @@ __global__ void __launch_bounds__(kThreads, 2) encode_kernel(const __grid_consta
 // decode (materialise) kernel
 // ---------------------------------------------------------------------------
 
-// int8 code -> exact f32 via the 2^23 magic (no I2F on the conversion pipe)
-__device__ __forceinline__ float i8_to_f32(uint32_t word_x80, int byte) {
-  return __uint_as_float(__byte_perm(word_x80, 0x4B000000u, 0x7650 + byte)) - 8388736.0f;
-}
 
 template <typename TOut>
 __device__ void k_decode_item(const DecodeArgs& a, int layer, int item, int lane) {
@@ -691,21 +642,6 @@ __device__ void k_decode_item(const DecodeArgs& a, int layer, int item, int lane
   }
 }
 
-// x / f32(sqrt(D)), correctly rounded. Power-of-four D: exact multiply.
-// Otherwise q = x*r corrected once with the exact FMA remainder; the
-// sequence is verified exhaustively over all f32 mantissas by
-// pkv_selftest(PKV_SELFTEST_DIVISION) and falls back to IEEE division
-// outside the normal range.
-template <int D>
-__device__ __forceinline__ float div_sqrt_d(float x, float c, float r) {
-  constexpr bool pow4 = (VG<D>::LOG2D % 2) == 0;
-  if (pow4) return x * r;
-  const float q = x * r;
-  const float e = fmaf(-q, c, x);
-  const float q1 = fmaf(e, r, q);
-  // the correction turns -0 / c into +0; the quotient has the sign of x
-  return __uint_as_float((__float_as_uint(q1) & 0x7fffffffu) | (__float_as_uint(x) & 0x80000000u));
-}
 
 template <int D, typename TOut, bool SIGN>
 __device__ void v_decode_item(const DecodeArgs& a, int layer, int item, int warp, int lane,
@@ -876,56 +812,11 @@ namespace {
 
 using namespace pkv;
 
-bool pinned_midpoints(const double* c, double* mid) {
-  for (int i = 0; i < 8; ++i)
-    if (!std::isfinite(c[i])) return false;
-  for (int i = 0; i < 7; ++i) {
-    if (!(c[i + 1] > c[i])) return false;
-    // largest double not above the exact rational midpoint
-    // (valuequant.py:62-71): TwoSum gives the exact a+b = s + e.
-    const double x = c[i], y = c[i + 1];
-    const double s = x + y;
-    const double bb = s - x;
-    const double e = (x - (s - bb)) + (y - bb);
-    double m = s * 0.5;
-    if (e < 0.0) m = std::nextafter(m, -INFINITY);
-    mid[i] = m;
-  }
-  return true;
-}
 
-bool fill_codebook(const double* centroids, Codebook3& cb) {
-  if (!centroids) return false;
-  if (!pinned_midpoints(centroids, cb.mid64)) return false;
-  for (int i = 0; i < 7; ++i) cb.mid32[i] = (float)cb.mid64[i];
-  for (int i = 0; i < 8; ++i) cb.cent32[i] = (float)centroids[i];
-  bool sym = true;
-  for (int i = 0; i < 8; ++i) sym = sym && centroids[i] == -centroids[7 - i];
-  cb.symmetric = sym ? 1 : 0;
-  return true;
-}
 
-int log2i(int d) {
-  int l = 0;
-  while ((1 << l) < d) ++l;
-  return l;
-}
 
-// Proven bound on |z32 - z_exact| for the fp32 fast path plus the error of
-// the f32 thresholds, with a 1.5x margin.
-float guard_delta(int d) {
-  const double u = std::ldexp(1.0, -24);
-  return (float)(1.5 * u * (log2i(d) * std::sqrt((double)d) + 6.0) + 1e-12);
-}
 
-bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
-int sm_count() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
 
 int blocks_per_sm(const void* fn) {
   int per_sm = 1;
@@ -996,16 +887,6 @@ int dispatch_decode(DecodeArgs& a, cudaStream_t st, bool do_v, bool sign) {
   }
 }
 
-bool fill_sign(const uint32_t* sign_bits_host, int d, uint32_t* dst) {
-  std::memset(dst, 0, 8 * sizeof(uint32_t));
-  if (!sign_bits_host) return false;
-  const int words = (d + 31) / 32;
-  bool any = false;
-  for (int i = 0; i < words && i < 8; ++i) dst[i] = sign_bits_host[i];
-  if (d % 32) dst[words - 1] &= (1u << (d % 32)) - 1u;
-  for (int i = 0; i < 8; ++i) any = any || dst[i] != 0;
-  return any;
-}
 
 template <int D>
 int v_items_for(long long nvec) {
@@ -1032,6 +913,15 @@ uintptr_t packed_align(int d) {
 
 }  // namespace
 
+namespace {
+// PKV_CODEC_PATH=warp forces the warp-granular kernels (debug / A-B timing).
+bool stream_enabled() {
+  const char* e = std::getenv("PKV_CODEC_PATH");
+  return !(e && std::strcmp(e, "warp") == 0);
+}
+bool stream_fallback(int rc) { return rc == PKV_ERR_ALIGNMENT || rc == PKV_ERR_UNSUPPORTED_HEAD_DIM; }
+}  // namespace
+
 extern "C" {
 
 int pkv_abi_version(void) { return PKV_ABI_VERSION; }
@@ -1053,10 +943,11 @@ int pkv_v_head_dim_supported(int d) {
   return d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256;
 }
 
-size_t pkv_encode_workspace_bytes(int num_layers) {
-  if (num_layers < 0) return 0;
+size_t pkv_encode_workspace_bytes(int num_layers, int64_t num_vectors, int head_dim) {
+  if (num_layers < 0 || num_vectors < 0 || head_dim < 1) return 0;
   const int l = std::min(num_layers, (int)PKV_MAX_LAYERS_PER_LAUNCH);
-  return (size_t)(2 * l + 2) * sizeof(uint32_t);
+  const size_t warp_path = (size_t)(2 * l + 2) * sizeof(uint32_t);
+  return std::max(warp_path, stream::workspace_bytes(l, num_vectors, head_dim));
 }
 
 int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
@@ -1072,7 +963,8 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
   const bool do_k = k_in != nullptr, do_v = v_in != nullptr;
   if (num_layers == 0 || num_vectors == 0 || (!do_k && !do_v)) return PKV_OK;
   if (do_v && !pkv_v_head_dim_supported(head_dim)) return PKV_ERR_UNSUPPORTED_HEAD_DIM;
-  if (workspace_bytes < pkv_encode_workspace_bytes(num_layers) || !workspace) return PKV_ERR_WORKSPACE;
+  if (workspace_bytes < pkv_encode_workspace_bytes(num_layers, num_vectors, head_dim) || !workspace)
+    return PKV_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long long nelem = (long long)num_vectors * head_dim;
 
@@ -1117,6 +1009,32 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
           return PKV_ERR_ALIGNMENT;
       }
     }
+    if (stream_enabled()) {
+      stream::EncodeRequest q;
+      std::memset(&q, 0, sizeof(q));
+      q.num_layers = L;
+      q.num_vectors = num_vectors;
+      q.head_dim = head_dim;
+      q.in_dtype = in_dtype;
+      q.k_mode = k_mode;
+      q.k_in = do_k ? k_in + l0 : nullptr;
+      q.v_in = do_v ? v_in + l0 : nullptr;
+      q.k_codes = do_k ? k_codes + l0 : nullptr;
+      q.k_scale = (do_k && k_scale) ? k_scale + l0 : nullptr;
+      q.k_bscale = (do_k && k_bscale) ? k_bscale + l0 : nullptr;
+      q.v_packed = do_v ? v_packed + l0 : nullptr;
+      q.v_scales = do_v ? v_scales + l0 : nullptr;
+      q.cb = a.cb;
+      std::memcpy(q.sign_bits, a.sign_bits, sizeof(q.sign_bits));
+      q.sign = sign;
+      q.status = status + l0;
+      q.replay_count = replay_count;
+      q.ws = workspace;
+      q.ws_bytes = workspace_bytes;
+      const int src = stream::encode(q, st);
+      if (src == PKV_OK) continue;
+      if (!stream_fallback(src)) return src;
+    }
     a.vec_ok = ok ? 1 : 0;
     const int k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;
     a.e_items = k_items;
@@ -1139,7 +1057,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     }
     a.round_start[a.num_rounds] = acc;
     a.total_items = acc;
-    if (cudaMemsetAsync(workspace, 0, pkv_encode_workspace_bytes(L), st) != cudaSuccess) return PKV_ERR_CUDA;
+    if (cudaMemsetAsync(workspace, 0, (size_t)(2 * L + 2) * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
     const bool sym = do_v ? a.cb.symmetric != 0 : true;
     const int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st, do_v, sym, sign)
                                        : dispatch_encode<__nv_bfloat16>(a, st, do_v, sym, sign);
@@ -1198,6 +1116,28 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
         if (!a.v_packed[l] || !a.v_scales[l] || !a.v_out[l]) return PKV_ERR_INVALID_ARG;
         if (!aligned(a.v_out[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim))) return PKV_ERR_ALIGNMENT;
       }
+    }
+    if (stream_enabled()) {
+      stream::DecodeRequest q;
+      std::memset(&q, 0, sizeof(q));
+      q.num_layers = L;
+      q.num_vectors = num_vectors;
+      q.head_dim = head_dim;
+      q.out_dtype = out_dtype;
+      q.k_mode = k_mode;
+      q.k_codes = do_k ? k_codes + l0 : nullptr;
+      q.k_scale = (do_k && k_scale) ? k_scale + l0 : nullptr;
+      q.k_bscale = (do_k && k_bscale) ? k_bscale + l0 : nullptr;
+      q.k_out = do_k ? k_out + l0 : nullptr;
+      q.v_packed = do_v ? v_packed + l0 : nullptr;
+      q.v_scales = do_v ? v_scales + l0 : nullptr;
+      q.v_out = do_v ? v_out + l0 : nullptr;
+      std::memcpy(q.cent32, a.cent32, sizeof(q.cent32));
+      std::memcpy(q.sign_bits, a.sign_bits, sizeof(q.sign_bits));
+      q.sign = sign;
+      const int src = stream::decode(q, st);
+      if (src == PKV_OK) continue;
+      if (!stream_fallback(src)) return src;
     }
     a.vec_ok = ok ? 1 : 0;
     a.k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;

@@ -1,0 +1,154 @@
+// Codec pieces shared by the warp-granular kernels (codec.cu) and the
+// TMA-streamed kernels (stream_codec.cu): exact key coding, the decode
+// division sequence, and host-side codebook / sign / guard-band setup.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "../../include/polykv.h"
+#include "pkv_common.cuh"
+
+namespace pkv {
+
+struct Codebook3 {
+  float mid32[7];
+  float cent32[8];
+  double mid64[7];
+  int symmetric;
+};
+
+constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
+
+constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
+
+// Reference formula (keyquant.py:61-64), evaluated exactly as numpy does in
+// fp64: q = f64(x)/scale, code = floor(|q| + 0.5) * sign(q), clipped.
+__device__ __forceinline__ int key_code_exact(float x, float s, int lo, int hi) {
+  double q = (double)x / (double)s;
+  double r = floor(fabs(q) + 0.5);
+  if (q < 0.0) r = -r;
+  if (r < lo) r = lo;
+  if (r > hi) r = hi;
+  return (int)r;
+}
+
+// 8 key codes of one chunk. Fast path: q = x * (1/s) rounded to nearest via
+// the 2^23 magic; the low byte of the magic sum is the two's-complement code.
+// Elements within kKeyEps of a half-point fall back to the exact formula.
+template <bool CLIP>
+__device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float rcp, bool force_exact) {
+  float m[8];
+  float worst = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float q = x[j] * rcp;
+    if (CLIP) q = fminf(fmaxf(q, -127.f), 127.f);
+    m[j] = q + kMagic;
+    const float n = m[j] - kMagic;
+    worst = fmaxf(worst, fabsf(q - n));
+  }
+  uint2 w;
+  w.x = __byte_perm(__byte_perm(__float_as_uint(m[0]), __float_as_uint(m[1]), 0x0040),
+                    __byte_perm(__float_as_uint(m[2]), __float_as_uint(m[3]), 0x0040), 0x5410);
+  w.y = __byte_perm(__byte_perm(__float_as_uint(m[4]), __float_as_uint(m[5]), 0x0040),
+                    __byte_perm(__float_as_uint(m[6]), __float_as_uint(m[7]), 0x0040), 0x5410);
+  if (force_exact || worst > 0.5f - kKeyEps) {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, CLIP ? -127 : -128, 127) & 0xffu);
+    w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+    w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
+  }
+  return w;
+}
+
+// int8 code -> exact f32 via the 2^23 magic (no I2F on the conversion pipe)
+__device__ __forceinline__ float i8_to_f32(uint32_t word_x80, int byte) {
+  return __uint_as_float(__byte_perm(word_x80, 0x4B000000u, 0x7650 + byte)) - 8388736.0f;
+}
+
+// x / f32(sqrt(D)), correctly rounded. Power-of-four D: exact multiply.
+// Otherwise q = x*r corrected once with the exact FMA remainder; the
+// sequence is verified exhaustively over all f32 mantissas by
+// pkv_selftest(PKV_SELFTEST_DIVISION) and falls back to IEEE division
+// outside the normal range.
+template <int D>
+__device__ __forceinline__ float div_sqrt_d(float x, float c, float r) {
+  constexpr bool pow4 = (VG<D>::LOG2D % 2) == 0;
+  if (pow4) return x * r;
+  const float q = x * r;
+  const float e = fmaf(-q, c, x);
+  const float q1 = fmaf(e, r, q);
+  // the correction turns -0 / c into +0; the quotient has the sign of x
+  return __uint_as_float((__float_as_uint(q1) & 0x7fffffffu) | (__float_as_uint(x) & 0x80000000u));
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+static inline bool pinned_midpoints(const double* c, double* mid) {
+  for (int i = 0; i < 8; ++i)
+    if (!std::isfinite(c[i])) return false;
+  for (int i = 0; i < 7; ++i) {
+    if (!(c[i + 1] > c[i])) return false;
+    // largest double not above the exact rational midpoint
+    // (valuequant.py:62-71): TwoSum gives the exact a+b = s + e.
+    const double x = c[i], y = c[i + 1];
+    const double s = x + y;
+    const double bb = s - x;
+    const double e = (x - (s - bb)) + (y - bb);
+    double m = s * 0.5;
+    if (e < 0.0) m = std::nextafter(m, -INFINITY);
+    mid[i] = m;
+  }
+  return true;
+}
+
+static inline bool fill_codebook(const double* centroids, Codebook3& cb) {
+  if (!centroids) return false;
+  if (!pinned_midpoints(centroids, cb.mid64)) return false;
+  for (int i = 0; i < 7; ++i) cb.mid32[i] = (float)cb.mid64[i];
+  for (int i = 0; i < 8; ++i) cb.cent32[i] = (float)centroids[i];
+  bool sym = true;
+  for (int i = 0; i < 8; ++i) sym = sym && centroids[i] == -centroids[7 - i];
+  cb.symmetric = sym ? 1 : 0;
+  return true;
+}
+
+static inline int log2i(int d) {
+  int l = 0;
+  while ((1 << l) < d) ++l;
+  return l;
+}
+
+// Proven bound on |z32 - z_exact| for the fp32 fast path plus the error of
+// the f32 thresholds, with a 1.5x margin.
+static inline float guard_delta(int d) {
+  const double u = std::ldexp(1.0, -24);
+  return (float)(1.5 * u * (log2i(d) * std::sqrt((double)d) + 6.0) + 1e-12);
+}
+
+static inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+static inline int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+static inline bool fill_sign(const uint32_t* sign_bits_host, int d, uint32_t* dst) {
+  std::memset(dst, 0, 8 * sizeof(uint32_t));
+  if (!sign_bits_host) return false;
+  const int words = (d + 31) / 32;
+  bool any = false;
+  for (int i = 0; i < words && i < 8; ++i) dst[i] = sign_bits_host[i];
+  if (d % 32) dst[words - 1] &= (1u << (d % 32)) - 1u;
+  for (int i = 0; i < 8; ++i) any = any || dst[i] != 0;
+  return any;
+}
+
+}  // namespace pkv

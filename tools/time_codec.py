@@ -11,7 +11,11 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--kmode", default="tensor")
+ap.add_argument("--path", default="stream", choices=["stream", "warp"])
 a = ap.parse_args()
+import os
+if a.path == 'warp':
+    os.environ['PKV_CODEC_PATH'] = 'warp'
 L, H, D, T = {"c3": (32, 8, 128, 4096), "c2": (24, 32, 64, 1851), "c1": (24, 32, 64, 600)}[a.config]
 dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
 g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
@@ -43,5 +47,5 @@ n = g.elements_per_tensor * L
 inb = 2 if a.dtype == "bf16" else 4
 bytes_ = {"enc_k": n * (inb + 1), "enc_v": n * (inb + 3 / 8) + 4 * n / D, "dec_k": 3 * n, "dec_v": n * (2 + 3 / 8) + 4 * n / D}
 bytes_["enc_kv"] = bytes_["enc_k"] + bytes_["enc_v"]; bytes_["dec_kv"] = bytes_["dec_k"] + bytes_["dec_v"]
-print(json.dumps({k: {"ms": round(v, 4), "GBs": round(bytes_[k] / v / 1e6, 1)} for k, v in res.items()}))
+print(a.config, a.dtype, a.path, json.dumps({k: {"ms": round(v, 4), "GBs": round(bytes_[k] / v / 1e6, 1)} for k, v in res.items()}))
 print("replays", int(arena.replay.item()))
