@@ -26,6 +26,7 @@
 // tickets and every CTA is resident, so the wait always terminates.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/polykv.h"
@@ -36,13 +37,23 @@
 namespace pkv {
 namespace stream {
 
-constexpr int kGroups = 2;
 constexpr int kWarpsPerGroup = 4;
 constexpr int kGroupThreads = 32 * kWarpsPerGroup;
-constexpr int kThreads = 32 + kGroups * kGroupThreads;  // producer warp + consumers
-constexpr int kChunk = 16384;                            // elements per work item
-constexpr int kRingBytes = 192 * 1024;
+constexpr int kEncGroups = 3;
+constexpr int kEncChunk = 16384;  // elements per encode work item
+constexpr int kDecChunk = 8192;   // elements per decode work item
+constexpr int kEncRingBytes = 192 * 1024;
 constexpr int kMaxL = kMaxLayers;
+
+template <int NG>
+constexpr int threads_for() {
+  return 32 + NG * kGroupThreads;  // producer warp + consumer groups
+}
+constexpr int kEncThreads = threads_for<kEncGroups>() + 32;  // + layer-max watcher warp
+template <typename TOut>
+constexpr int dec_groups() {
+  return sizeof(TOut) == 2 ? 3 : 2;
+}
 
 enum ItemKind : int { kEnd = 0, kAbsmax = 1, kKeyEnc = 2, kValEnc = 3, kKeyDec = 4, kValDec = 5 };
 
@@ -53,21 +64,36 @@ struct Item {
   int pad;
 };
 
-// Geometry of a head-vector tile of kChunk elements (VR vectors of D) held
-// as TMA boxes of BR rows x IB bytes (IB = swizzle span), NCB boxes across a
-// row and NRB boxes down.
-template <int D, int EB>
+// How a head vector of D coordinates maps onto lanes: TPV lanes per vector
+// (2 at d=128 so a lane holds at most 64 coordinates), lane = s * VPW + r for
+// vector r of the warp's pass and half s; the lane owns the contiguous
+// coordinates [s * CPT, (s + 1) * CPT).
+template <int D>
+struct VL {
+  static constexpr int TPV = D == 128 ? 2 : 1;
+  static constexpr int CPT = D / TPV;   // coordinates per lane
+  static constexpr int NCL = CPT / 8;   // 8-coordinate chunks per lane
+  static constexpr int NP = CPT / 2;    // f32 pairs per lane
+  static constexpr int VPW = 32 / TPV;  // vectors per warp pass
+  static constexpr int PB = 3 * D / 8;  // packed bytes per vector
+  static constexpr int PBL = PB / TPV;  // packed bytes per lane
+};
+
+// Geometry of a head-vector tile of CHUNK elements (VR vectors of D) held as
+// TMA boxes of BR rows x IB bytes (IB = swizzle span), NCB boxes across a row
+// and NRB boxes down.
+template <int D, int EB, int CHUNK>
 struct Tile {
-  static constexpr int RB = D * EB;                  // bytes per head vector
-  static constexpr int IB = RB < 128 ? RB : 128;     // inner box bytes
+  static constexpr int RB = D * EB;               // bytes per head vector
+  static constexpr int IB = RB < 128 ? RB : 128;  // inner box bytes
   static constexpr int NCB = RB / IB;
-  static constexpr int VR = kChunk / D;              // vectors per item
-  static constexpr int BR = VR < 256 ? VR : 256;     // rows per box
+  static constexpr int VR = CHUNK / D;            // vectors per item
+  static constexpr int BR = VR < 256 ? VR : 256;  // rows per box
   static constexpr int NRB = VR / BR;
   static constexpr int BOX_BYTES = BR * IB;
-  static constexpr int PASSES = VR / kGroupThreads;  // lane-per-vector passes per item
-  static constexpr int PB = 3 * D / 8;               // packed bytes per vector
-  static_assert(VR % kGroupThreads == 0, "item must hold a multiple of 128 vectors");
+  static constexpr int PER_PASS = kWarpsPerGroup * VL<D>::VPW;
+  static constexpr int PASSES = VR / PER_PASS;
+  static_assert(VR % PER_PASS == 0, "item must hold whole passes");
   // byte offset of 16-byte unit u of vector vr inside the tile
   __device__ __forceinline__ static uint32_t off(int vr, int u) {
     constexpr int UPB = IB / 16;  // units per box row
@@ -81,21 +107,19 @@ struct EncArgs {
   int num_layers, head_dim, k_mode, in_bytes;
   long long nvec, nelem;
   int nA, nE, nV;  // items per layer
-  int lag;         // E(l) items are issued in round l + lag
+  int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys
   unsigned int total;
   float delta;
   Codebook3 cb;
   uint32_t sign_bits[8];
   uint32_t* status;
   uint32_t* replay_count;
-  // Per-tensor key maxima are published without fences: every absmax item
-  // stores ONE 64-bit word (valid flag << 32 | max bits), so a reader that
-  // sees the flag sees the value (single-copy atomicity of aligned 64-bit
-  // accesses). The first key-encode item that finds all of a layer's words
-  // valid caches the layer maximum in layer_max[l] the same way.
-  unsigned long long* slots;      // [L][nA]
-  unsigned long long* layer_max;  // [L]
-  unsigned int* ticket;
+  // Per-tensor key maxima (keyquant.py:55): every CTA folds the absmax items
+  // it processed into one value per layer and publishes it once:
+  // atomicMax(layer_max[l]) -> fence -> ++layer_done[l]. A layer is ready when
+  // layer_done[l] == gridDim.x; only the producer warps look at these words.
+  unsigned int* layer_max;   // [L] max |K| bits
+  unsigned int* layer_done;  // [L] CTAs that have published
   const void* k_in[kMaxL];
   const void* v_in[kMaxL];
   int8_t* k_codes[kMaxL];
@@ -122,11 +146,6 @@ struct DecArgs {
   const float* v_scales[kMaxL];
 };
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -141,14 +160,14 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, f2(-1.f, -1.f), a); }
 
 // ---------------------------------------------------------------------------
-// Sylvester FWHT of one head vector held by one lane as D/2 f32 pairs:
+// Sylvester FWHT over N contiguous coordinates held as N/2 f32 pairs:
 //   xp[(c >> 1) * 8 + e] = (x[8c + e], x[8c + 8 + e])   for even c.
-// Stages run half = 1, 2, 4, ..., D/2 with lo' = lo + hi, hi' = lo - hi,
+// Stages run half = 1, 2, 4, ..., N/2 with lo' = lo + hi, hi' = lo - hi,
 // exactly kvpool/fwht.py:31-39, so every output is bit-identical to numpy.
 // ---------------------------------------------------------------------------
-template <int D>
+template <int N>
 __device__ __forceinline__ void fwht_pairs(float2* xp) {
-  constexpr int NP = D / 2;
+  constexpr int NP = N / 2;
 #pragma unroll
   for (int h = 1; h < 8; h <<= 1) {  // coordinate bits 0..2
 #pragma unroll
@@ -178,17 +197,33 @@ __device__ __forceinline__ void fwht_pairs(float2* xp) {
   }
 }
 
-// coordinate index of pair p, half hh
+// Rotation of one head vector: the lane-local stages, then (two lanes per
+// vector) the last stage half = D/2 across the lane pair: the lower half
+// keeps lo + hi = mine + partner, the upper half lo - hi = partner - mine;
+// fma(+-1, mine, partner) rounds exactly like numpy's add / subtract.
 template <int D>
-__device__ __forceinline__ constexpr int coord_of(int p, int hh) {
-  return ((p >> 3) * 2 + hh) * 8 + (p & 7);
+__device__ __forceinline__ void fwht_vector(float2* xp, int s) {
+  using G = VL<D>;
+  fwht_pairs<G::CPT>(xp);
+  if constexpr (G::TPV == 2) {
+    const float sg = s ? -1.f : 1.f;
+#pragma unroll
+    for (int p = 0; p < G::NP; ++p) {
+      const float px = __shfl_xor_sync(0xffffffffu, xp[p].x, G::VPW);
+      const float py = __shfl_xor_sync(0xffffffffu, xp[p].y, G::VPW);
+      xp[p] = __ffma2_rn(f2(sg, sg), xp[p], f2(px, py));
+    }
+  }
 }
 
-template <int D>
-__device__ __forceinline__ void apply_sign(float2* xp, const uint32_t* bits) {
+// coordinate (within the lane's CPT) of pair p, half hh
+__device__ __forceinline__ constexpr int coord_of(int p, int hh) { return ((p >> 3) * 2 + hh) * 8 + (p & 7); }
+
+template <int NP>
+__device__ __forceinline__ void apply_sign(float2* xp, const uint32_t* bits, int base) {
 #pragma unroll
-  for (int p = 0; p < D / 2; ++p) {
-    const int i0 = coord_of<D>(p, 0), i1 = coord_of<D>(p, 1);
+  for (int p = 0; p < NP; ++p) {
+    const int i0 = base + coord_of(p, 0), i1 = base + coord_of(p, 1);
     xp[p].x = __uint_as_float(__float_as_uint(xp[p].x) ^ (((bits[i0 >> 5] >> (i0 & 31)) & 1u) << 31));
     xp[p].y = __uint_as_float(__float_as_uint(xp[p].y) ^ (((bits[i1 >> 5] >> (i1 & 31)) & 1u) << 31));
   }
@@ -213,8 +248,8 @@ __device__ __forceinline__ void lds_chunk8<float>(uint32_t a0, uint32_t a1, floa
 // Exact fp64 replay of kvpool.valuequant.quantize_v for one head vector,
 // executed by the whole warp; writes the packed bytes and the scale.
 template <int D, typename TIn>
-__device__ __noinline__ void v_replay_staged(const EncArgs& a, const TIn* src, uint8_t* out_packed,
-                                             float* out_scale, double* R, uint8_t* C) {
+__device__ __noinline__ void v_replay(const EncArgs& a, const TIn* src, uint8_t* out_packed, float* out_scale,
+                                      double* R, uint8_t* C) {
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < D; i += 32) {
     double x = (double)load1(src + i);
@@ -262,38 +297,6 @@ __device__ __noinline__ void v_replay_staged(const EncArgs& a, const TIn* src, u
   __syncwarp();
 }
 
-// pack NW 24-bit words (chunk order) and store them at shared address `dst`
-template <int NW>
-__device__ __forceinline__ void sts_words(uint32_t dst, const uint32_t (&w)[NW]) {
-  if constexpr (NW % 4 == 0) {
-    uint32_t u[3 * NW / 4];
-#pragma unroll
-    for (int i = 0; i < NW / 4; ++i) {
-      u[3 * i + 0] = w[4 * i] | (w[4 * i + 1] << 24);
-      u[3 * i + 1] = (w[4 * i + 1] >> 8) | (w[4 * i + 2] << 16);
-      u[3 * i + 2] = (w[4 * i + 2] >> 16) | (w[4 * i + 3] << 8);
-    }
-    if constexpr (NW == 16) {
-      tma::sts128(dst, make_uint4(u[0], u[1], u[2], u[3]));
-      tma::sts128(dst + 16, make_uint4(u[4], u[5], u[6], u[7]));
-      tma::sts128(dst + 32, make_uint4(u[8], u[9], u[10], u[11]));
-    } else if constexpr (NW == 8) {
-      tma::sts64(dst, make_uint2(u[0], u[1]));
-      tma::sts64(dst + 8, make_uint2(u[2], u[3]));
-      tma::sts64(dst + 16, make_uint2(u[4], u[5]));
-    } else {
-      tma::sts32(dst, u[0]);
-      tma::sts32(dst + 4, u[1]);
-      tma::sts32(dst + 8, u[2]);
-    }
-  } else {  // NW == 2: 6 bytes, 2-byte aligned
-    const uint32_t lo = w[0] | (w[1] << 24), hi = w[1] >> 8;
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)(lo & 0xffff)) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst + 2), "h"((unsigned short)(lo >> 16)) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst + 4), "h"((unsigned short)(hi & 0xffff)) : "memory");
-  }
-}
-
 // pack NW 24-bit words (chunk order) and store them at global address `dst`
 template <int NW>
 __device__ __forceinline__ void stg_words(uint8_t* dst, const uint32_t (&w)[NW]) {
@@ -329,31 +332,34 @@ __device__ __forceinline__ void stg_words(uint8_t* dst, const uint32_t (&w)[NW])
 }
 
 // ---------------------------------------------------------------------------
-// encode: value item (VR head vectors), one lane per vector
+// encode: value item (VR head vectors)
 // ---------------------------------------------------------------------------
 template <int D, typename TIn, bool SYM, bool SIGN>
 __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, int wig, int lane, double* R,
                                uint8_t* C) {
-  using TL = Tile<D, (int)sizeof(TIn)>;
-  constexpr int NCH = D / 8, NP = D / 2;
+  using G = VL<D>;
+  using TL = Tile<D, (int)sizeof(TIn), kEncChunk>;
+  constexpr int NP = G::NP, NCL = G::NCL;
+  const int r = lane % G::VPW, s = lane / G::VPW;
   const long long vbase = (long long)it.idx * TL::VR;
   const float* m = a.cb.mid32;
   const float delta = a.delta;
-  uint8_t* gpk = a.v_packed[it.layer] + vbase * TL::PB;
+  uint8_t* gpk = a.v_packed[it.layer] + vbase * G::PB;
   float* gsc = a.v_scales[it.layer] + vbase;
 #pragma unroll 1
   for (int pass = 0; pass < TL::PASSES; ++pass) {
-    const int vr = pass * kGroupThreads + wig * 32 + lane;
+    const int vr = pass * TL::PER_PASS + wig * G::VPW + r;
     const long long v = vbase + vr;
     const bool valid = v < a.nvec;
     float2 xp[NP];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NCL; ++c) {
       float t[8];
+      const int gc = s * NCL + c;  // chunk index within the vector
       if constexpr (sizeof(TIn) == 2) {
-        lds_chunk8<TIn>(in_s + TL::off(vr, c), 0, t);
+        lds_chunk8<TIn>(in_s + TL::off(vr, gc), 0, t);
       } else {
-        lds_chunk8<TIn>(in_s + TL::off(vr, 2 * c), in_s + TL::off(vr, 2 * c + 1), t);
+        lds_chunk8<TIn>(in_s + TL::off(vr, 2 * gc), in_s + TL::off(vr, 2 * gc + 1), t);
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -363,15 +369,18 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
     }
     // squared norm in fp64 from the inputs (the rotation is orthogonal);
     // every x^2 is exact in fp64 and the sum is good to ~D * 2^-53.
-    double s0 = 0.0, s1 = 0.0;
+    double sacc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sacc[k] = 0.0;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      s0 = fma((double)xp[p].x, (double)xp[p].x, s0);
-      s1 = fma((double)xp[p].y, (double)xp[p].y, s1);
+      sacc[(2 * p) & 3] = fma((double)xp[p].x, (double)xp[p].x, sacc[(2 * p) & 3]);
+      sacc[(2 * p + 1) & 3] = fma((double)xp[p].y, (double)xp[p].y, sacc[(2 * p + 1) & 3]);
     }
-    const double S = s0 + s1;
-    if (SIGN) apply_sign<D>(xp, a.sign_bits);
-    fwht_pairs<D>(xp);  // U = H x (unnormalised)
+    double S = (sacc[0] + sacc[1]) + (sacc[2] + sacc[3]);
+    if constexpr (G::TPV == 2) S += __shfl_xor_sync(0xffffffffu, S, G::VPW);  // a + b == b + a
+    if (SIGN) apply_sign<NP>(xp, a.sign_bits, s * G::CPT);
+    fwht_vector<D>(xp, s);  // U = H x (unnormalised)
 
     bool replay = false, nonfinite = false, zero = false;
     float scale = 0.f, N = 0.f;
@@ -382,33 +391,39 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
     } else if (S < 0x1p-200 || S > 0x1p+200) {
       replay = true;
     } else {
-      const double r = sqrt(S * (1.0 / D));  // S/D is exact (D = 2^k)
-      scale = (float)r;
+      const double rr = sqrt(S * (1.0 / D));  // S/D is exact (D = 2^k)
+      scale = (float)rr;
       const double fd = (double)scale;
-      const float nb = (r >= fd) ? nextafterf(scale, INFINITY) : nextafterf(scale, 0.f);
+      const float nb = (rr >= fd) ? nextafterf(scale, INFINITY) : nextafterf(scale, 0.f);
       const double half_ulp = fabs((double)nb - fd) * 0.5;
-      if (half_ulp - fabs(r - fd) <= 1e-12 * r) replay = true;  // f32 rounding of the scale in doubt
+      if (half_ulp - fabs(rr - fd) <= 1e-12 * rr) replay = true;  // f32 rounding of the scale in doubt
       N = (float)sqrt(S);  // ||x||; z = U / ||x||
     }
 
-    uint32_t words[NCH];
+    uint32_t words[NCL];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) words[c] = 0;
+    for (int c = 0; c < NCL; ++c) words[c] = 0;
     if (SYM) {
       // thresholds folded into the U domain: |z| > t  <=>  |U| > t * ||x||
       const float2 T1 = f2(-m[4] * N, -m[4] * N), T2 = f2(-m[5] * N, -m[5] * N), T3 = f2(-m[6] * N, -m[6] * N);
       const float DL = delta * N;
-      float g = INFINITY;
+      // distance to the nearest decision threshold (0 included); 4
+      // independent min-accumulators keep the FMNMX3 chains short
+      float gacc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gacc[k] = INFINITY;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         const float2 u = xp[p];
         const float2 au = f2(fabsf(u.x), fabsf(u.y));
         const float2 d1 = __fadd2_rn(au, T1), d2 = __fadd2_rn(au, T2), d3 = __fadd2_rn(au, T3);
-        g = fminf(g, fminf(fabsf(d1.x), fabsf(d1.y)));
-        g = fminf(g, fminf(fabsf(d2.x), fabsf(d2.y)));
-        g = fminf(g, fminf(fabsf(d3.x), fabsf(d3.y)));
-        g = fminf(g, fminf(au.x, au.y));
-        // m = #thresholds above |u|; code = neg ? m : 7 - m
+        float& ga = gacc[(2 * p) & 3];
+        float& gb = gacc[(2 * p + 1) & 3];
+        ga = fminf(ga, fminf(fabsf(d1.x), fabsf(d1.y)));
+        gb = fminf(gb, fminf(fabsf(d2.x), fabsf(d2.y)));
+        ga = fminf(ga, fminf(fabsf(d3.x), fabsf(d3.y)));
+        gb = fminf(gb, fminf(au.x, au.y));
+        // mm = #thresholds above |u|; code = negative ? mm : 7 - mm
         const uint32_t mx = (__float_as_uint(d1.x) >> 31) + (__float_as_uint(d2.x) >> 31) + (__float_as_uint(d3.x) >> 31);
         const uint32_t my = (__float_as_uint(d1.y) >> 31) + (__float_as_uint(d2.y) >> 31) + (__float_as_uint(d3.y) >> 31);
         const uint32_t cx = (mx ^ ~(uint32_t)((int32_t)__float_as_uint(u.x) >> 31)) & 7u;
@@ -417,6 +432,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         words[c0] |= cx << (3 * e);
         words[c0 + 1] |= cy << (3 * e);
       }
+      const float g = fminf(fminf(gacc[0], gacc[1]), fminf(gacc[2], gacc[3]));
       replay |= g < DL;
     } else {
       const float inv = N > 0.f ? 1.0f / N : 0.f;
@@ -439,27 +455,27 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
     }
     if (zero || nonfinite) {
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) words[c] = 0;
+      for (int c = 0; c < NCL; ++c) words[c] = 0;
       scale = 0.f;
     }
+    if constexpr (G::TPV == 2) replay |= __shfl_xor_sync(0xffffffffu, (int)replay, G::VPW) != 0;
     replay = replay && valid && !nonfinite && !zero;
-    if (valid && nonfinite) atomicOr(&a.status[it.layer], PKV_FLAG_V_NONFINITE);
+    if (valid && nonfinite && s == 0) atomicOr(&a.status[it.layer], PKV_FLAG_V_NONFINITE);
     if (valid && !replay) {
-      stg_words<NCH>(gpk + vr * TL::PB, words);
-      gsc[vr] = scale;
+      stg_words<NCL>(gpk + vr * G::PB + s * G::PBL, words);
+      if (s == 0) gsc[vr] = scale;
     }
     // rare: exact fp64 replay, one vector at a time, whole warp
-    unsigned mask = __ballot_sync(0xffffffffu, replay);
+    unsigned mask = __ballot_sync(0xffffffffu, replay && s == 0);
     while (mask) {
       const int src_lane = __ffs(mask) - 1;
       mask &= mask - 1;
-      const int rvr = pass * kGroupThreads + wig * 32 + src_lane;
+      const int rvr = pass * TL::PER_PASS + wig * G::VPW + src_lane;
       const TIn* src = static_cast<const TIn*>(a.v_in[it.layer]) + (vbase + rvr) * D;
-      v_replay_staged<D, TIn>(a, src, gpk + rvr * TL::PB, gsc + rvr, R, C);
+      v_replay<D, TIn>(a, src, gpk + rvr * G::PB, gsc + rvr, R, C);
     }
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // encode: key items
@@ -482,52 +498,27 @@ __device__ __forceinline__ uint32_t lds_absmax8<float>(uint32_t a) {
 }
 
 template <typename TIn>
-__device__ void enc_absmax_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane,
-                                uint32_t* warp_max) {
-  const long long e0 = (long long)it.idx * kChunk;
-  const int n = (int)min((long long)kChunk, a.nelem - e0);
+__device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt) {
+  const long long e0 = (long long)it.idx * kEncChunk;
+  const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   uint32_t m = 0;
 #pragma unroll 4
-  for (int i = 0; i < kChunk / 8 / kGroupThreads; ++i) {
+  for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
     if (u * 8 < n) m = max(m, lds_absmax8<TIn>(in_s + u * 8 * (int)sizeof(TIn)));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) *warp_max = m;  // combined and published after the group barrier
+  return m;
 }
 
 template <typename TIn>
 __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane) {
-  const long long e0 = (long long)it.idx * kChunk;
-  const int n = (int)min((long long)kChunk, a.nelem - e0);
+  const long long e0 = (long long)it.idx * kEncChunk;
+  const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
   if (a.k_mode == PKV_K_TENSOR) {
-    unsigned long long lw = ld_relaxed64(a.layer_max + it.layer);
-    if (!(lw >> 32)) {
-      const unsigned long long* sl = a.slots + (long long)it.layer * a.nA;
-      uint32_t spins = 0;
-      uint64_t t0 = 0;
-      for (;;) {
-        bool all = true;
-        uint32_t m = 0;
-        for (int j = lane; j < a.nA; j += 32) {
-          const unsigned long long v = ld_relaxed64(sl + j);
-          all = all && (v >> 32) != 0;
-          m = max(m, (uint32_t)v);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (__all_sync(0xffffffffu, all)) {
-          lw = (1ull << 32) | m;
-          if (lane == 0) st_relaxed64(a.layer_max + it.layer, lw);
-          break;
-        }
-        __nanosleep(200);
-        tma::watchdog(spins, t0);
-      }
-    }
-    const uint32_t pb = (uint32_t)lw;
+    const uint32_t pb = (uint32_t)it.pad;  // layer max |K| bits, resolved by the producer
     const bool nonfinite = pb >= 0x7f800000u;
     const float s = (nonfinite || pb == 0) ? 0.f : __uint_as_float(pb) / 127.0f;  // f32(peak/127), keyquant.py:60
     if (it.idx == 0 && gt == 0) {
@@ -537,7 +528,7 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     const float rcp = 1.0f / s;
     const bool exact_all = !(s >= 1e-30f);
 #pragma unroll 4
-    for (int i = 0; i < kChunk / 8 / kGroupThreads; ++i) {
+    for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
       const int u = i * kGroupThreads + gt;
       if (u * 8 >= n) continue;
       float x[8];
@@ -549,7 +540,7 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
   // block32: one fp16 scale per 32 contiguous elements; 4 consecutive lanes own a block
   __half* bsc = a.k_bscale[it.layer];
 #pragma unroll 2
-  for (int i = 0; i < kChunk / 8 / kGroupThreads; ++i) {
+  for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
     const bool valid = u * 8 < n;
     float x[8];
@@ -591,14 +582,14 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
 // ---------------------------------------------------------------------------
 template <typename TOut>
 __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, uint8_t* out, int gt) {
-  const long long e0 = (long long)it.idx * kChunk;
-  const int n = (int)min((long long)kChunk, a.nelem - e0);
+  const long long e0 = (long long)it.idx * kDecChunk;
+  const int n = (int)min((long long)kDecChunk, a.nelem - e0);
   const bool tensor = a.k_mode == PKV_K_TENSOR;
   const float ts = tensor ? __ldg(a.k_scale[it.layer]) : 0.f;
   const __half* bsc = a.k_bscale[it.layer];
   const uint32_t out_s = tma::smem_u32(out);
 #pragma unroll 4
-  for (int i = 0; i < kChunk / 8 / kGroupThreads; ++i) {
+  for (int i = 0; i < kDecChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
     if (u * 8 >= n) continue;
     const uint2 w = tma::lds64(in_s + u * 8);
@@ -621,10 +612,9 @@ __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, ui
   }
 }
 
-// packed words of one vector (chunk order) from shared or global memory
-template <int D>
-__device__ __forceinline__ void load_packed(const uint8_t* p, bool smem, uint32_t (&w)[D / 8]) {
-  constexpr int NW = D / 8;
+// NW packed 24-bit words (chunk order) from shared or global memory
+template <int NW>
+__device__ __forceinline__ void load_packed(const uint8_t* p, bool smem, uint32_t (&w)[NW]) {
   if constexpr (NW % 4 == 0) {
     constexpr int NU = 3 * NW / 4;
     uint32_t u[NU];
@@ -663,29 +653,32 @@ __device__ __forceinline__ void load_packed(const uint8_t* p, bool smem, uint32_
 template <int D, typename TOut, bool SIGN>
 __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, int in_packed_bytes,
                                int in_scale_bytes, uint8_t* out, float* tbl, int gt, int wig, int lane) {
-  using TL = Tile<D, (int)sizeof(TOut)>;
-  constexpr int NCH = D / 8, NP = D / 2;
+  using G = VL<D>;
+  using TL = Tile<D, (int)sizeof(TOut), kDecChunk>;
+  constexpr int NCL = G::NCL, NP = G::NP;
+  const int r = lane % G::VPW, s = lane / G::VPW;
   const long long vbase = (long long)it.idx * TL::VR;
-  const uint8_t* gpk = a.v_packed[it.layer] + vbase * TL::PB;
+  const uint8_t* gpk = a.v_packed[it.layer] + vbase * G::PB;
   const float* gsc = a.v_scales[it.layer] + vbase;
-  const float* ssc = reinterpret_cast<const float*>(in + 3 * kChunk / 8);
+  const float* ssc = reinterpret_cast<const float*>(in + 3 * kDecChunk / 8);
   const uint32_t out_s = tma::smem_u32(out);
   const float2 c2 = f2(a.sqrt_d32, a.sqrt_d32), r2 = f2(a.rcp_sqrt_d32, a.rcp_sqrt_d32);
   char* tb = reinterpret_cast<char*>(tbl);
   const uint32_t lane_off = (uint32_t)gt * 4u;
 #pragma unroll 1
   for (int pass = 0; pass < TL::PASSES; ++pass) {
-    const int vr = pass * kGroupThreads + wig * 32 + lane;
+    const int vr = pass * TL::PER_PASS + wig * G::VPW + r;
     const bool valid = vbase + vr < a.nvec;
-    uint32_t words[NCH];
+    uint32_t words[NCL];
     float sc = 0.f;
     if (valid) {
-      const bool pk_smem = (vr + 1) * TL::PB <= in_packed_bytes;
-      load_packed<D>(pk_smem ? in + vr * TL::PB : gpk + vr * TL::PB, pk_smem, words);
+      const int o = vr * G::PB + s * G::PBL;
+      const bool pk_smem = o + G::PBL <= in_packed_bytes;
+      load_packed<NCL>(pk_smem ? in + o : gpk + o, pk_smem, words);
       sc = (vr + 1) * 4 <= in_scale_bytes ? ssc[vr] : __ldg(gsc + vr);
     } else {
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) words[j] = 0;
+      for (int j = 0; j < NCL; ++j) words[j] = 0;
     }
     // per-lane table of the 8 scaled centroids: table_f32[code] * scale
     // (valuequant.py:232-234), laid out [code][thread] -> conflict-free
@@ -693,7 +686,7 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
     for (int k = 0; k < 8; ++k) tbl[k * kGroupThreads + gt] = a.cent32[k] * sc;
     float2 xp[NP];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NCL; ++c) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         // byte address (code << 9) | lane_off   (kGroupThreads * 4 == 512)
@@ -704,7 +697,7 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
         else xp[(c >> 1) * 8 + e].x = val;
       }
     }
-    fwht_pairs<D>(xp);
+    fwht_vector<D>(xp, s);
     // / f32(sqrt(d)) (fwht.py:50): correctly rounded via one FMA correction
     // (exact for power-of-four d); scale == 0 or tiny -> IEEE division keeps
     // the signs of zeros and subnormal quotients.
@@ -724,22 +717,22 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
 #pragma unroll
       for (int p = 0; p < NP; ++p) xp[p] = f2(__fdiv_rn(xp[p].x, a.sqrt_d32), __fdiv_rn(xp[p].y, a.sqrt_d32));
     }
-    if (SIGN) apply_sign<D>(xp, a.sign_bits);
+    if (SIGN) apply_sign<NP>(xp, a.sign_bits, s * G::CPT);
     // swizzled staging of the output tile (TMA tensor store layout)
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const int p0 = (c >> 1) * 8;
+    for (int c = 0; c < NCL; ++c) {
+      const int p0 = (c >> 1) * 8, gc = s * NCL + c;
       float y[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) y[e] = (c & 1) ? xp[p0 + e].y : xp[p0 + e].x;
       if constexpr (sizeof(TOut) == 2) {
-        tma::sts128(out_s + TL::off(vr, c), make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
-                                                       pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7])));
+        tma::sts128(out_s + TL::off(vr, gc), make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
+                                                        pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7])));
       } else {
-        tma::sts128(out_s + TL::off(vr, 2 * c), make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]),
-                                                           __float_as_uint(y[2]), __float_as_uint(y[3])));
-        tma::sts128(out_s + TL::off(vr, 2 * c + 1), make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]),
-                                                               __float_as_uint(y[6]), __float_as_uint(y[7])));
+        tma::sts128(out_s + TL::off(vr, 2 * gc), make_uint4(__float_as_uint(y[0]), __float_as_uint(y[1]),
+                                                            __float_as_uint(y[2]), __float_as_uint(y[3])));
+        tma::sts128(out_s + TL::off(vr, 2 * gc + 1), make_uint4(__float_as_uint(y[4]), __float_as_uint(y[5]),
+                                                                __float_as_uint(y[6]), __float_as_uint(y[7])));
       }
     }
   }
@@ -748,43 +741,23 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
 // ---------------------------------------------------------------------------
 // ticket -> item
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ long long enc_round_start(const EncArgs& a, int r) {
-  const int L = a.num_layers;
-  const long long er = min(max(r - a.lag, 0), L);
-  return (long long)min(r, L) * (a.nA + a.nV) + er * a.nE;
-}
-
-// Round r holds A(r) [r < L], then V(r) [r < L] interleaved with E(r - lag)
-// [lag <= r < L + lag].
-__device__ __forceinline__ Item enc_item(const EncArgs& a, unsigned int t) {
-  const int L = a.num_layers;
-  int lo = 0, hi = L + a.lag;  // find the last r with start(r) <= t
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (enc_round_start(a, mid) <= (long long)t) lo = mid;
-    else hi = mid;
-  }
-  const int r = lo;
-  long long off = (long long)t - enc_round_start(a, r);
-  const long long nAr = r < L ? a.nA : 0, nVr = r < L ? a.nV : 0;
-  const long long nEr = (r >= a.lag && r - a.lag < L) ? a.nE : 0;
+// Encode work lists (each CTA walks a static round-robin slice of both):
+//   AV list: per layer l, the absmax items A(l, *) then the value items V(l, *);
+//   E list:  per layer l, the key-encode items E(l, *).
+// The producer issues E(l, *) only once layer l's maximum is known, so
+// consumers never wait on another CTA.
+__device__ __forceinline__ Item av_item(const EncArgs& a, long long t) {
+  const long long per = (long long)a.nA + a.nV;
   Item it{kEnd, 0, 0, 0};
-  if (off < nAr) {
-    it.kind = kAbsmax; it.layer = r; it.idx = (int)off;
-    return it;
+  it.layer = (int)(t / per);
+  const long long off = t - (long long)it.layer * per;
+  if (off < a.nA) {
+    it.kind = kAbsmax;
+    it.idx = (int)off;
+  } else {
+    it.kind = kValEnc;
+    it.idx = (int)(off - a.nA);
   }
-  off -= nAr;
-  const long long both = 2 * min(nVr, nEr);
-  if (off < both) {
-    if ((off & 1) == 0) { it.kind = kValEnc; it.layer = r; }
-    else { it.kind = kKeyEnc; it.layer = r - a.lag; }
-    it.idx = (int)(off >> 1);
-    return it;
-  }
-  off -= both;
-  if (nVr > nEr) { it.kind = kValEnc; it.layer = r; }
-  else { it.kind = kKeyEnc; it.layer = r - a.lag; }
-  it.idx = (int)(min(nVr, nEr) + off);
   return it;
 }
 
@@ -806,51 +779,55 @@ __device__ __forceinline__ Item dec_item(const DecArgs& a, unsigned int t) {
 }
 
 // ---------------------------------------------------------------------------
-// shared-memory plan
+// shared-memory plans
 // ---------------------------------------------------------------------------
-// Encode: a ring of input stages only (outputs are small and go straight to
-// global memory). Decode: a ring of input stages plus NOB output buffers per
-// consumer group, written back by TMA stores.
+// Every consumer group owns a private ring of NSG input stages, so a slow item
+// (a layer-max wait, an fp64 replay) only ever stalls its own group. Encode
+// outputs are small and go straight to global memory; decode outputs are
+// staged in two buffers per group and written back by TMA stores.
+constexpr int kMaxGroups = 3;
+constexpr int kMaxSG = 4;
+
 template <int EB_IN>
 struct EncPlan {
-  static constexpr int IN = kChunk * EB_IN;
-  static constexpr int STAGE = IN;
-  static constexpr int NST = kRingBytes / STAGE;
-  static_assert(NST >= 2 && NST <= 8, "ring depth");
+  static constexpr int NG = kEncGroups;
+  static constexpr int STAGE = kEncChunk * EB_IN;
+  static constexpr int NSG = kEncRingBytes / STAGE / NG;  // stages per group
+  static_assert(NSG >= 1 && NSG <= kMaxSG, "ring depth");
 };
-template <int EB_OUT>
+template <int EB_OUT, int NG_>
 struct DecPlan {
-  static constexpr int IN = kChunk;  // >= key codes, packed values + scales
-  static constexpr int STAGE = IN;
-  static constexpr int OUT = kChunk * EB_OUT;
-  static constexpr int NOB = EB_OUT == 2 ? 2 : 1;  // output buffers per group
-  static constexpr int OUT_TOTAL = kGroups * NOB * OUT;
-  static constexpr int NST = (208 * 1024 - OUT_TOTAL) / STAGE;
-  static_assert(NST >= 2 && NST <= 8, "ring depth");
+  static constexpr int NG = NG_;
+  static constexpr int STAGE = kDecChunk;  // >= key codes, packed values + scales
+  static constexpr int OUT = kDecChunk * EB_OUT;
+  static constexpr int NOB = 2;            // output buffers per group
+  static constexpr int OUT_TOTAL = NG * NOB * OUT;
+  static constexpr int NSG = 3;
+  static_assert(OUT_TOTAL + NG * NSG * STAGE <= 200 * 1024, "decode shared memory");
 };
 
 struct alignas(8) Ctl {
-  uint64_t full[8];
-  uint64_t empty[8];
-  Item items[8];
-  uint32_t warp_max[kGroups][kWarpsPerGroup];
+  uint64_t full[kMaxGroups][kMaxSG];
+  uint64_t empty[kMaxGroups][kMaxSG];
+  Item items[kMaxGroups][kMaxSG];
+  uint32_t amax[kMaxGroups][kMaxSG][kWarpsPerGroup];  // absmax item results
+  uint32_t cta_max[kMaxL];                             // encode producer: per-layer fold
+  int a_left[kMaxL];                                   // absmax items of this CTA still open
+  volatile int pub_ready[kMaxL];                       // producer -> watcher: fold complete
+  volatile uint32_t ready_max[kMaxL];                  // watcher -> producer: layer max bits
+  volatile int ready_count;                            // layers [0, ready_count) are ready
 };
-
-template <int D>
-constexpr int replay_bytes() {
-  return kGroups * kWarpsPerGroup * (D * 8 + D);
-}
 
 template <int D, typename TIn>
 constexpr size_t enc_smem_bytes() {
-  return 1024 + (size_t)EncPlan<(int)sizeof(TIn)>::NST * EncPlan<(int)sizeof(TIn)>::STAGE + sizeof(Ctl) +
-         replay_bytes<D>();
+  using P = EncPlan<(int)sizeof(TIn)>;
+  return 1024 + (size_t)P::NG * P::NSG * P::STAGE + sizeof(Ctl) + (size_t)P::NG * kWarpsPerGroup * (D * 8 + D);
 }
 template <typename TOut>
 constexpr size_t dec_smem_bytes() {
-  using P = DecPlan<(int)sizeof(TOut)>;
-  return 1024 + (size_t)P::OUT_TOTAL + (size_t)P::NST * P::STAGE + sizeof(Ctl) +
-         kGroups * 8 * kGroupThreads * sizeof(float);
+  using P = DecPlan<(int)sizeof(TOut), dec_groups<TOut>()>;
+  return 1024 + (size_t)P::OUT_TOTAL + (size_t)P::NG * P::NSG * P::STAGE + sizeof(Ctl) +
+         (size_t)P::NG * 8 * kGroupThreads * sizeof(float);
 }
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -858,99 +835,242 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + ((1024u - (s & 1023u)) & 1023u);
 }
 
+// Producer side of the per-group rings: hands out items to whichever group
+// has a free stage. next_item(t) maps ticket/slot t to an Item; issue(it, dst,
+// bar) starts its TMA loads.
+template <int NG, int NSG, class Next, class Issue>
+__device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes, Next next_item, Issue issue) {
+  int head[NG];
+  bool ended[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    head[g] = 0;
+    ended[g] = false;
+  }
+  int ends = 0;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  while (ends < NG) {
+    bool any = false;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      if (ended[g]) continue;
+      const int k = head[g] % NSG, use = head[g] / NSG;
+      if (use >= 1 && !tma::mbar_test_wait(&ctl->empty[g][k], (uint32_t)(use - 1) & 1u)) continue;
+      const Item it = next_item();
+      ctl->items[g][k] = it;
+      ++head[g];
+      any = true;
+      if (it.kind == kEnd) {
+        tma::mbar_arrive(&ctl->full[g][k]);
+        ended[g] = true;
+        ++ends;
+        continue;
+      }
+      issue(it, ring + (g * NSG + k) * stage_bytes, &ctl->full[g][k]);
+    }
+    if (!any) {
+      __nanosleep(32);
+      tma::watchdog(spins, t0);
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // encode kernel
 // ---------------------------------------------------------------------------
 template <int D, typename TIn, bool SYM, bool SIGN>
-__global__ void __launch_bounds__(kThreads, 1) enc_kernel(const __grid_constant__ EncArgs a) {
+__global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_constant__ EncArgs a) {
   using P = EncPlan<(int)sizeof(TIn)>;
+  using TL = Tile<D, (int)sizeof(TIn), kEncChunk>;
+  constexpr int NG = P::NG, NSG = P::NSG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = align1024(smem_raw);
-  Ctl* ctl = reinterpret_cast<Ctl*>(ring + P::NST * P::STAGE);
+  Ctl* ctl = reinterpret_cast<Ctl*>(ring + NG * NSG * P::STAGE);
   uint8_t* replay_base = reinterpret_cast<uint8_t*>(ctl + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = a.num_layers;
+  const long long G = gridDim.x, b = blockIdx.x;
+  const long long per = (long long)a.nA + a.nV;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < P::NST; ++s) {
-      tma::mbar_init(&ctl->full[s], 1);
-      tma::mbar_init(&ctl->empty[s], 1);
-    }
+    for (int g = 0; g < NG; ++g)
+      for (int k = 0; k < NSG; ++k) {
+        tma::mbar_init(&ctl->full[g][k], 1);
+        tma::mbar_init(&ctl->empty[g][k], kWarpsPerGroup);  // every warp releases
+      }
     tma::fence_mbar_init();
+    // this CTA's share of each layer's absmax items; layers it has none of
+    // can be published right away
+    for (int l = 0; l < L; ++l) {
+      const long long j0 = ((b - (long long)l * per) % G + G) % G;
+      ctl->a_left[l] = j0 < a.nA ? (int)((a.nA - 1 - j0) / G + 1) : 0;
+      ctl->cta_max[l] = 0;
+      ctl->pub_ready[l] = ctl->a_left[l] == 0 ? 1 : 0;
+    }
+    ctl->ready_count = a.nA > 0 ? 0 : L;
   }
   __syncthreads();
 
-  if (warp == 0) {
-    // ---------------- producer ----------------
-    if (lane == 0) {
-      const uint64_t pol_last = tma::policy_evict_last(), pol_first = tma::policy_evict_first();
-      unsigned int* ticket = a.ticket;
-      int ends = 0;
-      for (int seq = 0;; ++seq) {
-        const int s = seq % P::NST;
-        const uint32_t ph = (uint32_t)(seq / P::NST) & 1u;
-        if (seq >= P::NST) tma::mbar_wait(&ctl->empty[s], ph ^ 1u);
-        const unsigned int t = atomicAdd(ticket, 1u);
-        const Item it = t < a.total ? enc_item(a, t) : Item{kEnd, 0, 0, 0};
-        ctl->items[s] = it;
-        uint8_t* in = ring + s * P::STAGE;
-        if (it.kind == kEnd) {
-          tma::mbar_arrive(&ctl->full[s]);
-          if (++ends == kGroups) break;
-          continue;
+  if (warp == 1 + NG * kWarpsPerGroup) {
+    // ---------------- layer-max watcher ----------------
+    // Publishes this CTA's per-layer maxima (atomicMax -> fence -> arrival)
+    // and turns "all CTAs published" into a shared-memory ready count, so
+    // the producer never waits on a global-memory round trip.
+    if (lane == 0 && a.nA > 0) {
+      int next_pub = 0, next_ready = 0;
+      uint32_t spins = 0;
+      uint64_t t0 = 0;
+      while (next_ready < L || next_pub < L) {
+        bool any = false;
+        while (next_pub < L && ctl->pub_ready[next_pub]) {
+          if (ctl->a_left[next_pub] == 0 && ctl->cta_max[next_pub]) atomicMax(a.layer_max + next_pub, ctl->cta_max[next_pub]);
+          __threadfence();  // the maximum is visible before the arrival
+          atomicAdd(a.layer_done + next_pub, 1u);
+          ++next_pub;
+          any = true;
         }
-        if (it.kind == kValEnc) {
-          using TL = Tile<D, (int)sizeof(TIn)>;
-          tma::mbar_arrive_expect_tx(&ctl->full[s], (uint32_t)P::IN);
-          const int row0 = it.idx * TL::VR;
-#pragma unroll 1
-          for (int rb = 0; rb < TL::NRB; ++rb)
-#pragma unroll 1
-            for (int cb = 0; cb < TL::NCB; ++cb)
-              tma::tensor2d_g2s(in + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
-                                cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, &ctl->full[s], pol_first);
-        } else {
-          const long long e0 = (long long)it.idx * kChunk;
-          const uint32_t bytes = (uint32_t)(min((long long)kChunk, a.nelem - e0) * (long long)sizeof(TIn));
-          tma::mbar_arrive_expect_tx(&ctl->full[s], bytes);
-          const TIn* src = static_cast<const TIn*>(a.k_in[it.layer]) + e0;
-          tma::bulk_g2s(in, src, bytes, &ctl->full[s], it.kind == kAbsmax ? pol_last : pol_first);
+        if (next_ready < L &&
+            *reinterpret_cast<volatile const uint32_t*>(a.layer_done + next_ready) >= (uint32_t)G) {
+          __threadfence();
+          ctl->ready_max[next_ready] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + next_ready);
+          __threadfence_block();
+          ctl->ready_count = ++next_ready;
+          any = true;
+        }
+        if (!any) {
+          __nanosleep(128);
+          tma::watchdog(spins, t0);
         }
       }
     }
     return;
   }
 
-  // ---------------- consumers ----------------
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol_last = tma::policy_evict_last(), pol_first = tma::policy_evict_first();
+      const long long av_total = (long long)L * per, e_total = (long long)L * a.nE;
+      int a_open = 0;  // absmax items of this CTA not yet folded in
+      for (int l = 0; l < L; ++l) a_open += ctl->a_left[l];
+      long long t_av = b, t_e = b;
+      int head[NG], tail[NG];
+      bool ended[NG];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        head[g] = tail[g] = 0;
+        ended[g] = false;
+      }
+      int ends = 0;
+      uint32_t spins = 0;
+      uint64_t t0 = 0;
+      // keep going until every group has its END and every absmax result of
+      // this CTA is published (other CTAs' key items depend on it)
+      while (ends < NG || a_open > 0) {
+        bool any = false;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          // retire finished stages; fold absmax results and publish layers
+          while (tail[g] < head[g]) {
+            const int k = tail[g] % NSG;
+            if (!tma::mbar_test_wait(&ctl->empty[g][k], (uint32_t)(tail[g] / NSG) & 1u)) break;
+            const Item done = ctl->items[g][k];
+            if (done.kind == kAbsmax) {
+              uint32_t m = ctl->cta_max[done.layer];
+#pragma unroll
+              for (int w = 0; w < kWarpsPerGroup; ++w) m = max(m, ctl->amax[g][k][w]);
+              ctl->cta_max[done.layer] = m;
+              --a_open;
+              if (--ctl->a_left[done.layer] == 0) {
+                __threadfence_block();
+                ctl->pub_ready[done.layer] = 1;  // the watcher publishes it
+              }
+            }
+            ++tail[g];
+            any = true;
+          }
+          if (ended[g] || head[g] - tail[g] >= NSG) continue;
+          // next item for group g: a ready key-encode item first, else absmax / value
+          Item it{kEnd, 0, 0, 0};
+          if (t_e < e_total) {
+            const int le = (int)(t_e / a.nE);
+            if (le < ctl->ready_count) {
+              it.kind = kKeyEnc;
+              it.layer = le;
+              it.idx = (int)(t_e - (long long)le * a.nE);
+              if (a.k_mode == PKV_K_TENSOR) it.pad = (int)ctl->ready_max[le];
+              t_e += G;
+            }
+          }
+          if (it.kind == kEnd && t_av < av_total) {
+            it = av_item(a, t_av);
+            t_av += G;
+          }
+          if (it.kind == kEnd && t_e < e_total) continue;  // key items wait for their layer
+          const int k = head[g] % NSG;
+          ctl->items[g][k] = it;
+          ++head[g];
+          any = true;
+          if (it.kind == kEnd) {
+            tma::mbar_arrive(&ctl->full[g][k]);
+            ended[g] = true;
+            ++ends;
+            continue;
+          }
+          uint8_t* dst = ring + (g * NSG + k) * P::STAGE;
+          uint64_t* bar = &ctl->full[g][k];
+          if (it.kind == kValEnc) {
+            tma::mbar_arrive_expect_tx(bar, (uint32_t)P::STAGE);
+            const int row0 = it.idx * TL::VR;
+#pragma unroll 1
+            for (int rb = 0; rb < TL::NRB; ++rb)
+#pragma unroll 1
+              for (int cb = 0; cb < TL::NCB; ++cb)
+                tma::tensor2d_g2s(dst + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
+                                  cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
+          } else {
+            // absmax loads keep the key chunk in L2 (evict_last) for the
+            // key-encode item that re-reads it shortly after
+            const long long e0 = (long long)it.idx * kEncChunk;
+            const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
+            tma::mbar_arrive_expect_tx(bar, bytes);
+            const TIn* src = static_cast<const TIn*>(a.k_in[it.layer]) + e0;
+            tma::bulk_g2s(dst, src, bytes, bar, it.kind == kAbsmax ? pol_last : pol_first);
+          }
+        }
+        if (!any) {
+          __nanosleep(64);
+          tma::watchdog(spins, t0);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers (warps work independently) ----------------
   const int g = (warp - 1) / kWarpsPerGroup;
   const int wig = (warp - 1) % kWarpsPerGroup;
   const int gt = threadIdx.x - 32 - g * kGroupThreads;
   double* R = reinterpret_cast<double*>(replay_base) + (warp - 1) * D;
-  uint8_t* C = replay_base + kGroups * kWarpsPerGroup * D * 8 + (warp - 1) * D;
-  for (int seq = g;; seq += kGroups) {
-    const int s = seq % P::NST;
-    const uint32_t ph = (uint32_t)(seq / P::NST) & 1u;
-    tma::mbar_wait(&ctl->full[s], ph);
-    const Item it = ctl->items[s];
+  uint8_t* C = replay_base + NG * kWarpsPerGroup * D * 8 + (warp - 1) * D;
+  for (int n = 0;; ++n) {
+    const int k = n % NSG;
+    tma::mbar_wait(&ctl->full[g][k], (uint32_t)(n / NSG) & 1u);
+    const Item it = ctl->items[g][k];
     if (it.kind == kEnd) break;
-    const uint32_t in_s = tma::smem_u32(ring + s * P::STAGE);
+    const uint32_t in_s = tma::smem_u32(ring + (g * NSG + k) * P::STAGE);
+    const bool skip = a.dbg == 1 || (a.dbg == 2 && it.kind == kValEnc) || (a.dbg == 3 && it.kind != kValEnc);
     if (it.kind == kAbsmax) {
-      enc_absmax_item<TIn>(a, it, in_s, gt, lane, &ctl->warp_max[g][wig]);
+      const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
+      if (lane == 0) ctl->amax[g][k][wig] = m;  // folded by the producer
+    } else if (skip) {
     } else if (it.kind == kKeyEnc) {
       enc_key_item<TIn>(a, it, in_s, gt, lane);
     } else {
       enc_value_item<D, TIn, SYM, SIGN>(a, it, in_s, wig, lane, R, C);
     }
-    // every warp of the group is done reading the stage: hand it back
-    tma::named_bar_sync(1 + g, kGroupThreads);
-    if (gt == 0) {
-      tma::mbar_arrive(&ctl->empty[s]);
-      if (it.kind == kAbsmax) {
-        uint32_t m = 0;
-#pragma unroll
-        for (int w = 0; w < kWarpsPerGroup; ++w) m = max(m, ctl->warp_max[g][w]);
-        st_relaxed64(a.slots + (long long)it.layer * a.nA + it.idx, (1ull << 32) | m);
-      }
-    }
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);  // this warp is done with the stage
   }
 }
 
@@ -958,20 +1078,22 @@ __global__ void __launch_bounds__(kThreads, 1) enc_kernel(const __grid_constant_
 // decode kernel
 // ---------------------------------------------------------------------------
 template <int D, typename TOut, bool SIGN>
-__global__ void __launch_bounds__(kThreads, 1) dec_kernel(const __grid_constant__ DecArgs a) {
-  using P = DecPlan<(int)sizeof(TOut)>;
-  using TL = Tile<D, (int)sizeof(TOut)>;
+__global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kernel(const __grid_constant__ DecArgs a) {
+  using P = DecPlan<(int)sizeof(TOut), dec_groups<TOut>()>;
+  using TL = Tile<D, (int)sizeof(TOut), kDecChunk>;
+  constexpr int NG = P::NG, NSG = P::NSG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* obuf = align1024(smem_raw);  // 1024-aligned swizzled output tiles
   uint8_t* ring = obuf + P::OUT_TOTAL;
-  Ctl* ctl = reinterpret_cast<Ctl*>(ring + P::NST * P::STAGE);
+  Ctl* ctl = reinterpret_cast<Ctl*>(ring + NG * NSG * P::STAGE);
   float* tables = reinterpret_cast<float*>(ctl + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < P::NST; ++s) {
-      tma::mbar_init(&ctl->full[s], 1);
-      tma::mbar_init(&ctl->empty[s], 1);
-    }
+    for (int g = 0; g < NG; ++g)
+      for (int k = 0; k < NSG; ++k) {
+        tma::mbar_init(&ctl->full[g][k], 1);
+        tma::mbar_init(&ctl->empty[g][k], 1);
+      }
     tma::fence_mbar_init();
   }
   __syncthreads();
@@ -979,36 +1101,31 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_first = tma::policy_evict_first();
-      int ends = 0;
-      for (int seq = 0;; ++seq) {
-        const int s = seq % P::NST;
-        const uint32_t ph = (uint32_t)(seq / P::NST) & 1u;
-        if (seq >= P::NST) tma::mbar_wait(&ctl->empty[s], ph ^ 1u);
-        // static round-robin schedule: items are independent and near-uniform
-        const unsigned long long t64 = (unsigned long long)blockIdx.x + (unsigned long long)seq * gridDim.x;
-        const unsigned int t = t64 < a.total ? (unsigned int)t64 : a.total;
-        const Item it = t < a.total ? dec_item(a, t) : Item{kEnd, 0, 0, 0};
-        ctl->items[s] = it;
-        uint8_t* in = ring + s * P::STAGE;
-        if (it.kind == kEnd) {
-          tma::mbar_arrive(&ctl->full[s]);
-          if (++ends == kGroups) break;
-          continue;
-        }
+      // static slice of the item list per CTA; within the CTA items go to
+      // whichever group frees a stage first
+      unsigned long long t = blockIdx.x;
+      auto next_item = [&]() -> Item {
+        if (t >= a.total) return Item{kEnd, 0, 0, 0};
+        const Item it = dec_item(a, (unsigned int)t);
+        t += gridDim.x;
+        return it;
+      };
+      auto issue = [&](const Item& it, uint8_t* in, uint64_t* bar) {
         if (it.kind == kKeyDec) {
-          const long long e0 = (long long)it.idx * kChunk;
-          const uint32_t bytes = (uint32_t)min((long long)kChunk, a.nelem - e0);
-          tma::mbar_arrive_expect_tx(&ctl->full[s], bytes);
-          tma::bulk_g2s(in, a.k_codes[it.layer] + e0, bytes, &ctl->full[s], pol_first);
+          const long long e0 = (long long)it.idx * kDecChunk;
+          const uint32_t bytes = (uint32_t)min((long long)kDecChunk, a.nelem - e0);
+          tma::mbar_arrive_expect_tx(bar, bytes);
+          tma::bulk_g2s(in, a.k_codes[it.layer] + e0, bytes, bar, pol_first);
         } else {
           const long long v0 = (long long)it.idx * TL::VR;
           const int nv = (int)min((long long)TL::VR, a.nvec - v0);
-          const uint32_t pb = (uint32_t)(nv * TL::PB) & ~15u, sb = (uint32_t)(nv * 4) & ~15u;
-          tma::mbar_arrive_expect_tx(&ctl->full[s], pb + sb);
-          if (pb) tma::bulk_g2s(in, a.v_packed[it.layer] + v0 * TL::PB, pb, &ctl->full[s], pol_first);
-          if (sb) tma::bulk_g2s(in + 3 * kChunk / 8, a.v_scales[it.layer] + v0, sb, &ctl->full[s], pol_first);
+          const uint32_t pb = (uint32_t)(nv * VL<D>::PB) & ~15u, sb = (uint32_t)(nv * 4) & ~15u;
+          tma::mbar_arrive_expect_tx(bar, pb + sb);
+          if (pb) tma::bulk_g2s(in, a.v_packed[it.layer] + v0 * VL<D>::PB, pb, bar, pol_first);
+          if (sb) tma::bulk_g2s(in + 3 * kDecChunk / 8, a.v_scales[it.layer] + v0, sb, bar, pol_first);
         }
-      }
+      };
+      produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
     }
     return;
   }
@@ -1017,16 +1134,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(const __grid_constant_
   const int wig = (warp - 1) % kWarpsPerGroup;
   const int gt = threadIdx.x - 32 - g * kGroupThreads;
   float* tbl = tables + g * 8 * kGroupThreads;
-  int nitems = 0;
-  for (int seq = g;; seq += kGroups) {
-    const int s = seq % P::NST;
-    const uint32_t ph = (uint32_t)(seq / P::NST) & 1u;
-    tma::mbar_wait(&ctl->full[s], ph);
-    const Item it = ctl->items[s];
+  for (int n = 0;; ++n) {
+    const int k = n % NSG;
+    tma::mbar_wait(&ctl->full[g][k], (uint32_t)(n / NSG) & 1u);
+    const Item it = ctl->items[g][k];
     if (it.kind == kEnd) break;
-    uint8_t* in = ring + s * P::STAGE;
-    uint8_t* out = obuf + (g * P::NOB + (nitems % P::NOB)) * P::OUT;
-    ++nitems;
+    uint8_t* in = ring + (g * NSG + k) * P::STAGE;
+    uint8_t* out = obuf + (g * P::NOB + (n & 1)) * P::OUT;
     int nv = 0;
     long long v0 = 0;
     if (it.kind == kKeyDec) {
@@ -1034,16 +1148,16 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(const __grid_constant_
     } else {
       v0 = (long long)it.idx * TL::VR;
       nv = (int)min((long long)TL::VR, a.nvec - v0);
-      dec_value_item<D, TOut, SIGN>(a, it, in, (nv * TL::PB) & ~15, (nv * 4) & ~15, out, tbl, gt, wig, lane);
+      dec_value_item<D, TOut, SIGN>(a, it, in, (nv * VL<D>::PB) & ~15, (nv * 4) & ~15, out, tbl, gt, wig, lane);
     }
     tma::fence_proxy_async_smem();
-    if (P::NOB == 2 && gt == 0) tma::bulk_wait_read<0>();  // the other buffer is free for the next item
+    if (gt == 0) tma::bulk_wait_read<0>();  // the store of the previous item has left the other buffer
     tma::named_bar_sync(1 + g, kGroupThreads);
     if (gt == 0) {
-      tma::mbar_arrive(&ctl->empty[s]);  // inputs consumed
+      tma::mbar_arrive(&ctl->empty[g][k]);  // inputs consumed
       if (it.kind == kKeyDec) {
-        const long long e0 = (long long)it.idx * kChunk;
-        const int bytes = (int)min((long long)kChunk, a.nelem - e0) * (int)sizeof(TOut);
+        const long long e0 = (long long)it.idx * kDecChunk;
+        const int bytes = (int)min((long long)kDecChunk, a.nelem - e0) * (int)sizeof(TOut);
         tma::bulk_s2g(static_cast<TOut*>(a.k_out[it.layer]) + e0, out, (uint32_t)bytes);
       } else {
 #pragma unroll 1
@@ -1056,9 +1170,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(const __grid_constant_
         }
       }
       tma::bulk_commit();
-      if (P::NOB == 1) tma::bulk_wait_read<0>();
     }
-    if (P::NOB == 1) tma::named_bar_sync(1 + g, kGroupThreads);  // single buffer: wait for its read-out
   }
   if (gt == 0) tma::bulk_wait<0>();
 }
@@ -1090,10 +1202,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // [nvec, D] head-vector tensor of one layer as a 2-D TMA map with the box
 // geometry of Tile<D, eb>.
-bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec) {
+bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec, int chunk) {
   auto fn = encode_fn();
   if (!fn) return false;
-  const int RB = D * eb, IB = RB < 128 ? RB : 128, VR = kChunk / D, BR = VR < 256 ? VR : 256;
+  const int RB = D * eb, IB = RB < 128 ? RB : 128, VR = chunk / D, BR = VR < 256 ? VR : 256;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)nvec};
   cuuint64_t strides[1] = {(cuuint64_t)RB};
   cuuint32_t box[2] = {(cuuint32_t)(IB / eb), (cuuint32_t)BR};
@@ -1109,15 +1221,15 @@ bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec) {
 }
 
 template <typename K>
-int coop_launch(K kernel, const void* args, size_t smem, cudaStream_t st) {
+int coop_launch(K kernel, const void* args, size_t smem, int threads, cudaStream_t st) {
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PKV_ERR_CUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
     return PKV_ERR_CUDA;
   void* params[] = {const_cast<void*>(args)};
   const cudaError_t e =
-      cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)(sm_count() * per_sm)), dim3(kThreads), params,
+      cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)(sm_count() * per_sm)), dim3(threads), params,
                                   smem, st);
   return e == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
@@ -1126,11 +1238,11 @@ template <int D, typename TIn>
 int enc_launch_d(const EncArgs& a, bool sym, bool sign, cudaStream_t st) {
   const size_t smem = enc_smem_bytes<D, TIn>();
   if (sym) {
-    return sign ? coop_launch(enc_kernel<D, TIn, true, true>, &a, smem, st)
-                : coop_launch(enc_kernel<D, TIn, true, false>, &a, smem, st);
+    return sign ? coop_launch(enc_kernel<D, TIn, true, true>, &a, smem, kEncThreads, st)
+                : coop_launch(enc_kernel<D, TIn, true, false>, &a, smem, kEncThreads, st);
   }
-  return sign ? coop_launch(enc_kernel<D, TIn, false, true>, &a, smem, st)
-              : coop_launch(enc_kernel<D, TIn, false, false>, &a, smem, st);
+  return sign ? coop_launch(enc_kernel<D, TIn, false, true>, &a, smem, kEncThreads, st)
+              : coop_launch(enc_kernel<D, TIn, false, false>, &a, smem, kEncThreads, st);
 }
 
 template <typename TIn>
@@ -1147,8 +1259,8 @@ int enc_launch(const EncArgs& a, int d, bool sym, bool sign, cudaStream_t st) {
 template <int D, typename TOut>
 int dec_launch_d(const DecArgs& a, bool sign, cudaStream_t st) {
   const size_t smem = dec_smem_bytes<TOut>();
-  return sign ? coop_launch(dec_kernel<D, TOut, true>, &a, smem, st)
-              : coop_launch(dec_kernel<D, TOut, false>, &a, smem, st);
+  return sign ? coop_launch(dec_kernel<D, TOut, true>, &a, smem, threads_for<dec_groups<TOut>()>(), st)
+              : coop_launch(dec_kernel<D, TOut, false>, &a, smem, threads_for<dec_groups<TOut>()>(), st);
 }
 
 template <typename TOut>
@@ -1170,9 +1282,10 @@ bool head_dim_streamable(int d) { return d == 16 || d == 32 || d == 64 || d == 1
 
 size_t workspace_bytes(int num_layers, long long num_vectors, int head_dim) {
   const long long nelem = num_vectors * (long long)std::max(head_dim, 1);
-  const long long kch = (nelem + kChunk - 1) / kChunk;
+  const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
   const long long L = std::min(std::max(num_layers, 0), kMaxL);
-  return (size_t)(L * kch * 8 + L * 8 + 16);
+  (void)kch;
+  return (size_t)(L * 8 + 16);
 }
 
 int encode(const EncodeRequest& r, cudaStream_t st) {
@@ -1197,37 +1310,26 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   std::memcpy(a->sign_bits, r.sign_bits, sizeof(a->sign_bits));
   a->status = r.status;
   a->replay_count = r.replay_count;
-  // workspace: [u64 slots L*nA][u64 layer_max L][u32 ticket]
-  unsigned long long* w64 = reinterpret_cast<unsigned long long*>(r.ws);
-  const long long kch = (nelem + kChunk - 1) / kChunk;
-  const long long vch = (r.num_vectors + (kChunk / std::max(r.head_dim, 1)) - 1) / (kChunk / std::max(r.head_dim, 1));
+  const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
+  const long long vr = kEncChunk / std::max(r.head_dim, 1);
   a->nE = do_k ? (int)kch : 0;
   a->nA = (do_k && r.k_mode == PKV_K_TENSOR) ? (int)kch : 0;
-  a->nV = do_v ? (int)vch : 0;
+  a->nV = do_v ? (int)((r.num_vectors + vr - 1) / vr) : 0;
   const long long total = (long long)L * (a->nA + a->nE + a->nV);
-  if (total >= (1LL << 32) - 1024) {
+  if (total >= (1LL << 31)) {
     delete a;
     return PKV_ERR_INVALID_ARG;
   }
+  // workspace: [u32 layer_max L][u32 layer_done L]
+  unsigned int* w32 = reinterpret_cast<unsigned int*>(r.ws);
   a->total = (unsigned int)total;
-  a->slots = w64;
-  a->layer_max = w64 + (long long)L * a->nA;
-  a->ticket = reinterpret_cast<unsigned int*>(a->layer_max + L);
+  if (const char* dbg = std::getenv("PKV_DBG_ENC")) a->dbg = std::atoi(dbg);
+  a->layer_max = w32;
+  a->layer_done = w32 + L;
   const size_t ws_need = workspace_bytes(L, r.num_vectors, r.head_dim);
   if (r.ws_bytes < ws_need) {
     delete a;
     return PKV_ERR_ALIGNMENT;  // too small for this path: the caller falls back
-  }
-  // lag between a layer's absmax items and its key-encode items: about twice
-  // the items in flight in all rings, bounded so the lagged key tensors stay
-  // L2-resident (~40 MB).
-  {
-    const long long inflight = (long long)sm_count() * (eb == 2 ? EncPlan<2>::NST : EncPlan<4>::NST);
-    const long long round = std::max(1LL, (long long)a->nA + a->nV + a->nE);
-    long long lag = 1 + (2 * inflight + round - 1) / round;
-    const long long layer_bytes = std::max(1LL, nelem * eb);
-    lag = std::min(lag, std::max(1LL, (40LL << 20) / layer_bytes));
-    a->lag = (int)std::max(1LL, std::min(lag, (long long)L));
   }
   int rc = PKV_OK;
   for (int l = 0; l < L && rc == PKV_OK; ++l) {
@@ -1243,7 +1345,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       a->v_packed[l] = r.v_packed[l];
       a->v_scales[l] = r.v_scales[l];
       if (!a16(a->v_in[l]) || !a16(a->v_packed[l]) || !a16(a->v_scales[l])) rc = PKV_ERR_ALIGNMENT;
-      else if (!make_map(&a->tm_v[l], a->v_in[l], eb, r.head_dim, r.num_vectors)) rc = PKV_ERR_CUDA;
+      else if (!make_map(&a->tm_v[l], a->v_in[l], eb, r.head_dim, r.num_vectors, kEncChunk)) rc = PKV_ERR_CUDA;
     }
   }
   if (rc == PKV_OK && cudaMemsetAsync(r.ws, 0, ws_need, st) != cudaSuccess) rc = PKV_ERR_CUDA;
@@ -1275,8 +1377,8 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
   a->rcp_sqrt_d32 = 1.0f / a->sqrt_d32;
   std::memcpy(a->sign_bits, r.sign_bits, sizeof(a->sign_bits));
   std::memcpy(a->cent32, r.cent32, sizeof(a->cent32));
-  const long long kch = (nelem + kChunk - 1) / kChunk;
-  const long long vr = kChunk / std::max(r.head_dim, 1);
+  const long long kch = (nelem + kDecChunk - 1) / kDecChunk;
+  const long long vr = kDecChunk / std::max(r.head_dim, 1);
   a->nK = do_k ? (int)kch : 0;
   a->nV = do_v ? (int)((r.num_vectors + vr - 1) / vr) : 0;
   const long long total = (long long)L * (a->nK + a->nV);
@@ -1298,7 +1400,7 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
       a->v_packed[l] = r.v_packed[l];
       a->v_scales[l] = r.v_scales[l];
       if (!a16(a->v_packed[l]) || !a16(a->v_scales[l]) || !a16(r.v_out[l])) rc = PKV_ERR_ALIGNMENT;
-      else if (!make_map(&a->tm_v[l], r.v_out[l], eb, r.head_dim, r.num_vectors)) rc = PKV_ERR_CUDA;
+      else if (!make_map(&a->tm_v[l], r.v_out[l], eb, r.head_dim, r.num_vectors, kDecChunk)) rc = PKV_ERR_CUDA;
     }
   }
   if (rc == PKV_OK)
