@@ -214,10 +214,47 @@ def run_ours(args, cfg):
                       device=dev)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    none = [None] * L
+
+    def encode_k():
+        _encode_layers(ks, none, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
+
+    def encode_v():
+        _encode_layers(none, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
+
+    def capture(fn):
+        """CUDA-graph a launch sequence so the timed loop measures the GPU, not
+        the Python/ctypes enqueue path; None if capture is unavailable."""
+        if args.no_graph:
+            return None
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                fn()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                fn()
+            torch.cuda.synchronize(dev)
+            return gr.replay
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] graph capture unavailable ({exc}); timing eager launches", file=sys.stderr)
+            return None
+
     for _ in range(args.warmup):
         encode()
         decode()
     raise_for_status(arena.status)
+    torch.cuda.synchronize(dev)
+    run_enc = capture(encode) or encode
+    run_dec = capture(decode) or decode
+    run_enc_k = capture(encode_k) or encode_k
+    run_enc_v = capture(encode_v) or encode_v
+    graphed = not args.no_graph and run_enc is not encode
+    for _ in range(args.warmup):
+        run_enc()
+        run_dec()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -226,17 +263,31 @@ def run_ours(args, cfg):
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize(dev)
         start.record(stream)
-        for a, b, c in marks:
-            a.record(stream)
-            encode()
-            b.record(stream)
-            decode()
-            c.record(stream)
+        for a_, b_, c_ in marks:
+            a_.record(stream)
+            run_enc()
+            b_.record(stream)
+            run_dec()
+            c_.record(stream)
         end.record(stream)
         torch.cuda.synchronize(dev)
     total_ms = start.elapsed_time(end)
-    enc_ms = sum(a.elapsed_time(b) for a, b, _ in marks) / args.steps
-    dec_ms = sum(b.elapsed_time(c) for _, b, c in marks) / args.steps
+    enc_ms = sum(a_.elapsed_time(b_) for a_, b_, _ in marks) / args.steps
+    dec_ms = sum(b_.elapsed_time(c_) for _, b_, c_ in marks) / args.steps
+
+    def time_it(fn, n):
+        s_, e_ = ev(), ev()
+        fn()
+        torch.cuda.synchronize(dev)
+        s_.record(stream)
+        for _ in range(n):
+            fn()
+        e_.record(stream)
+        torch.cuda.synchronize(dev)
+        return s_.elapsed_time(e_) / n
+
+    enc_k_ms = time_it(run_enc_k, args.steps)
+    enc_v_ms = time_it(run_enc_v, args.steps)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -303,7 +354,15 @@ def run_ours(args, cfg):
                 "pool_gbs": pool_bytes / (a_ms / 1e3) / 1e9}
 
     peak, peak_kind = measured_peaks()
-    dom_ms, dom_bytes, dom_name = (enc_ms, comp_b, "encode_kernel") if enc_ms >= dec_ms else (dec_ms, deq_b, "decode_kernel")
+    n = g.elements_per_tensor
+    vecs = g.vectors_per_tensor
+    kb = 4 if args.k_mode == "tensor" else 2 * ((n + 31) // 32)
+    bytes_k = L * (n * in_b + n + kb)                      # key encode (absmax pass + codes)
+    bytes_v = L * (n * in_b + 3 * n / 8 + 4 * vecs)        # value encode
+    kernels = {"encode_values": (enc_v_ms, bytes_v), "encode_keys": (enc_k_ms, bytes_k),
+               "decode": (dec_ms, deq_b)}
+    dom_name = max(kernels, key=lambda k: kernels[k][0])
+    dom_ms, dom_bytes = kernels[dom_name]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     prof = ROOT / "profiles" / "traffic.json"
     traffic = None
@@ -337,11 +396,15 @@ def run_ours(args, cfg):
                        "l2": "inputs larger than L2 (no flush needed)",
                        "parallelism": f"replica x{world} (independent pools per GPU)"},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic},
             "kernels": {"encode_ms": enc_ms, "encode_gbs": comp_b / (enc_ms / 1e3) / 1e9,
                         "decode_ms": dec_ms, "decode_gbs": deq_b / (dec_ms / 1e3) / 1e9,
-                        "encode_bytes": comp_b, "decode_bytes": deq_b},
-            "gpu_launches": 2 * args.steps,
+                        "encode_values_ms": enc_v_ms, "encode_values_gbs": bytes_v / (enc_v_ms / 1e3) / 1e9,
+                        "encode_keys_ms": enc_k_ms, "encode_keys_gbs": bytes_k / (enc_k_ms / 1e3) / 1e9,
+                        "encode_bytes": comp_b, "decode_bytes": deq_b, "cuda_graph": graphed},
+            # per step: value-encode, key-absmax, key-encode, decode (+ one memset)
+            "gpu_launches": (4 if args.k_mode == "tensor" else 3) * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "decode_attention": attn,
@@ -357,7 +420,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
@@ -366,6 +429,7 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-attention", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graphs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

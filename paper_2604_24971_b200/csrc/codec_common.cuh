@@ -65,6 +65,32 @@ __device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float r
   return w;
 }
 
+// Branch-free fast path of key_chunk (keyquant.py:61-64) on f32 pairs:
+// q = x * (1/s) rounded to the nearest integer with the 2^23 magic (the low
+// byte of the magic sum is the two's-complement code). `bad` is set when any
+// element lies within kKeyEps of a rounding half-point; the caller then
+// re-codes the chunk with key_chunk(..., force_exact = true).
+__device__ __forceinline__ uint2 key_chunk_fast(const float (&x)[8], float2 rcp2, bool& bad) {
+  const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
+  uint32_t mb[8];
+  float worst = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 q = __fmul2_rn(make_float2(x[2 * j], x[2 * j + 1]), rcp2);
+    const float2 m = __fadd2_rn(q, mg);
+    const float2 n = __fadd2_rn(m, nmg);
+    const float2 d = __ffma2_rn(n, make_float2(-1.f, -1.f), q);  // q - n, exact
+    worst = fmaxf(worst, fmaxf(fabsf(d.x), fabsf(d.y)));
+    mb[2 * j] = __float_as_uint(m.x);
+    mb[2 * j + 1] = __float_as_uint(m.y);
+  }
+  bad = worst > 0.5f - kKeyEps;
+  uint2 w;
+  w.x = __byte_perm(__byte_perm(mb[0], mb[1], 0x0040), __byte_perm(mb[2], mb[3], 0x0040), 0x5410);
+  w.y = __byte_perm(__byte_perm(mb[4], mb[5], 0x0040), __byte_perm(mb[6], mb[7], 0x0040), 0x5410);
+  return w;
+}
+
 // int8 code -> exact f32 via the 2^23 magic (no I2F on the conversion pipe)
 __device__ __forceinline__ float i8_to_f32(uint32_t word_x80, int byte) {
   return __uint_as_float(__byte_perm(word_x80, 0x4B000000u, 0x7650 + byte)) - 8388736.0f;

@@ -17,13 +17,11 @@
 //     owns one head vector (no warp shuffles in the rotation) and still reads
 //     / writes its 16-byte chunks without bank conflicts.
 //
-// Encode work items, in ticket order, per round r = 0..L:
-//     A(r, *)  absmax of key chunk (per-tensor scale mode only), loaded with an
-//              L2 evict_last policy so the chunk stays resident,
-//     V(r, *) interleaved with E(r-1, *)  value chunks / key-encode chunks.
-// E(l, j) re-reads key chunk j of layer l (from L2) and waits until every
-// A(l, *) has published its maximum. All A(l, *) tickets precede all E(l, *)
-// tickets and every CTA is resident, so the wait always terminates.
+// Per-tensor key scales (keyquant.py:55) need max|K| over a whole layer
+// before any key code can be written. A short absmax pass over all layers
+// (absmax_kernel) runs first; the encode kernel then walks the layers in
+// REVERSE order so the key tensors the absmax pass touched last are still
+// L2-resident when they are re-read.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -49,7 +47,7 @@ template <int NG>
 constexpr int threads_for() {
   return 32 + NG * kGroupThreads;  // producer warp + consumer groups
 }
-constexpr int kEncThreads = threads_for<kEncGroups>() + 32;  // + layer-max watcher warp
+constexpr int kEncThreads = threads_for<kEncGroups>();
 template <typename TOut>
 constexpr int dec_groups() {
   return sizeof(TOut) == 2 ? 3 : 2;
@@ -106,7 +104,7 @@ struct EncArgs {
   CUtensorMap tm_v[kMaxL];  // value inputs, [nvec, D] per layer
   int num_layers, head_dim, k_mode, in_bytes;
   long long nvec, nelem;
-  int nA, nE, nV;  // items per layer
+  int nE, nV;  // items per layer
   int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys
   unsigned int total;
   float delta;
@@ -114,12 +112,7 @@ struct EncArgs {
   uint32_t sign_bits[8];
   uint32_t* status;
   uint32_t* replay_count;
-  // Per-tensor key maxima (keyquant.py:55): every CTA folds the absmax items
-  // it processed into one value per layer and publishes it once:
-  // atomicMax(layer_max[l]) -> fence -> ++layer_done[l]. A layer is ready when
-  // layer_done[l] == gridDim.x; only the producer warps look at these words.
-  unsigned int* layer_max;   // [L] max |K| bits
-  unsigned int* layer_done;  // [L] CTAs that have published
+  const unsigned int* layer_max;  // [L] max |K| bits from absmax_kernel
   const void* k_in[kMaxL];
   const void* v_in[kMaxL];
   int8_t* k_codes[kMaxL];
@@ -513,12 +506,13 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
 }
 
 template <typename TIn>
-__device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane) {
+__device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane,
+                             const uint32_t* layer_max) {
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
   if (a.k_mode == PKV_K_TENSOR) {
-    const uint32_t pb = (uint32_t)it.pad;  // layer max |K| bits, resolved by the producer
+    const uint32_t pb = layer_max[it.layer];  // from absmax_kernel (stream-ordered), staged in smem
     const bool nonfinite = pb >= 0x7f800000u;
     const float s = (nonfinite || pb == 0) ? 0.f : __uint_as_float(pb) / 127.0f;  // f32(peak/127), keyquant.py:60
     if (it.idx == 0 && gt == 0) {
@@ -527,13 +521,31 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     }
     const float rcp = 1.0f / s;
     const bool exact_all = !(s >= 1e-30f);
-#pragma unroll 4
-    for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
+    // branch-free fast pass over the whole item; chunks near a rounding
+    // half-point are re-coded exactly afterwards (rare)
+    constexpr int ITERS = kEncChunk / 8 / kGroupThreads;
+    uint32_t need = 0;
+#pragma unroll
+    for (int i = 0; i < ITERS; ++i) {
+      const int u = i * kGroupThreads + gt;
+      if (u * 8 < n) {
+        float x[8];
+        lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
+        bool bad;
+        st_u2(dst + u * 8, key_chunk_fast(x, make_float2(rcp, rcp), bad));
+        need |= (uint32_t)bad << i;
+      }
+    }
+    if (exact_all) need = (1u << ITERS) - 1u;
+#pragma unroll 1
+    while (need) {
+      const int i = __ffs(need) - 1;
+      need &= need - 1;
       const int u = i * kGroupThreads + gt;
       if (u * 8 >= n) continue;
       float x[8];
       lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
-      st_u2(dst + u * 8, key_chunk<false>(x, s, rcp, exact_all));
+      st_u2(dst + u * 8, key_chunk<false>(x, s, rcp, true));
     }
     return;
   }
@@ -741,22 +753,23 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
 // ---------------------------------------------------------------------------
 // ticket -> item
 // ---------------------------------------------------------------------------
-// Encode work lists (each CTA walks a static round-robin slice of both):
-//   AV list: per layer l, the absmax items A(l, *) then the value items V(l, *);
-//   E list:  per layer l, the key-encode items E(l, *).
-// The producer issues E(l, *) only once layer l's maximum is known, so
-// consumers never wait on another CTA.
-__device__ __forceinline__ Item av_item(const EncArgs& a, long long t) {
-  const long long per = (long long)a.nA + a.nV;
+// Encode work list: layers in reverse order; per layer the value items
+// V(l, *) interleaved with the key items E(l, *). CTA b takes items b, b + G,
+// b + 2G, ... (items are independent).
+__device__ __forceinline__ Item enc_item(const EncArgs& a, long long t) {
+  const long long per = (long long)a.nE + a.nV;
   Item it{kEnd, 0, 0, 0};
-  it.layer = (int)(t / per);
-  const long long off = t - (long long)it.layer * per;
-  if (off < a.nA) {
-    it.kind = kAbsmax;
-    it.idx = (int)off;
+  const int r = (int)(t / per);
+  it.layer = a.num_layers - 1 - r;
+  long long off = t - (long long)r * per;
+  const long long both = 2 * (long long)min(a.nE, a.nV);
+  if (off < both) {
+    it.kind = (off & 1) ? kKeyEnc : kValEnc;
+    it.idx = (int)(off >> 1);
   } else {
-    it.kind = kValEnc;
-    it.idx = (int)(off - a.nA);
+    off -= both;
+    it.kind = a.nE > a.nV ? kKeyEnc : kValEnc;
+    it.idx = (int)(min(a.nE, a.nV) + off);
   }
   return it;
 }
@@ -810,12 +823,7 @@ struct alignas(8) Ctl {
   uint64_t full[kMaxGroups][kMaxSG];
   uint64_t empty[kMaxGroups][kMaxSG];
   Item items[kMaxGroups][kMaxSG];
-  uint32_t amax[kMaxGroups][kMaxSG][kWarpsPerGroup];  // absmax item results
-  uint32_t cta_max[kMaxL];                             // encode producer: per-layer fold
-  int a_left[kMaxL];                                   // absmax items of this CTA still open
-  volatile int pub_ready[kMaxL];                       // producer -> watcher: fold complete
-  volatile uint32_t ready_max[kMaxL];                  // watcher -> producer: layer max bits
-  volatile int ready_count;                            // layers [0, ready_count) are ready
+  uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer (absmax_kernel ran before)
 };
 
 template <int D, typename TIn>
@@ -889,9 +897,6 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
   Ctl* ctl = reinterpret_cast<Ctl*>(ring + NG * NSG * P::STAGE);
   uint8_t* replay_base = reinterpret_cast<uint8_t*>(ctl + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L = a.num_layers;
-  const long long G = gridDim.x, b = blockIdx.x;
-  const long long per = (long long)a.nA + a.nV;
   if (threadIdx.x == 0) {
     for (int g = 0; g < NG; ++g)
       for (int k = 0; k < NSG; ++k) {
@@ -899,150 +904,39 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         tma::mbar_init(&ctl->empty[g][k], kWarpsPerGroup);  // every warp releases
       }
     tma::fence_mbar_init();
-    // this CTA's share of each layer's absmax items; layers it has none of
-    // can be published right away
-    for (int l = 0; l < L; ++l) {
-      const long long j0 = ((b - (long long)l * per) % G + G) % G;
-      ctl->a_left[l] = j0 < a.nA ? (int)((a.nA - 1 - j0) / G + 1) : 0;
-      ctl->cta_max[l] = 0;
-      ctl->pub_ready[l] = ctl->a_left[l] == 0 ? 1 : 0;
-    }
-    ctl->ready_count = a.nA > 0 ? 0 : L;
   }
+  if (threadIdx.x < a.num_layers && a.layer_max) ctl->layer_max[threadIdx.x] = __ldg(a.layer_max + threadIdx.x);
   __syncthreads();
-
-  if (warp == 1 + NG * kWarpsPerGroup) {
-    // ---------------- layer-max watcher ----------------
-    // Publishes this CTA's per-layer maxima (atomicMax -> fence -> arrival)
-    // and turns "all CTAs published" into a shared-memory ready count, so
-    // the producer never waits on a global-memory round trip.
-    if (lane == 0 && a.nA > 0) {
-      int next_pub = 0, next_ready = 0;
-      uint32_t spins = 0;
-      uint64_t t0 = 0;
-      while (next_ready < L || next_pub < L) {
-        bool any = false;
-        while (next_pub < L && ctl->pub_ready[next_pub]) {
-          if (ctl->a_left[next_pub] == 0 && ctl->cta_max[next_pub]) atomicMax(a.layer_max + next_pub, ctl->cta_max[next_pub]);
-          __threadfence();  // the maximum is visible before the arrival
-          atomicAdd(a.layer_done + next_pub, 1u);
-          ++next_pub;
-          any = true;
-        }
-        if (next_ready < L &&
-            *reinterpret_cast<volatile const uint32_t*>(a.layer_done + next_ready) >= (uint32_t)G) {
-          __threadfence();
-          ctl->ready_max[next_ready] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + next_ready);
-          __threadfence_block();
-          ctl->ready_count = ++next_ready;
-          any = true;
-        }
-        if (!any) {
-          __nanosleep(128);
-          tma::watchdog(spins, t0);
-        }
-      }
-    }
-    return;
-  }
 
   if (warp == 0) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      const uint64_t pol_last = tma::policy_evict_last(), pol_first = tma::policy_evict_first();
-      const long long av_total = (long long)L * per, e_total = (long long)L * a.nE;
-      int a_open = 0;  // absmax items of this CTA not yet folded in
-      for (int l = 0; l < L; ++l) a_open += ctl->a_left[l];
-      long long t_av = b, t_e = b;
-      int head[NG], tail[NG];
-      bool ended[NG];
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        head[g] = tail[g] = 0;
-        ended[g] = false;
-      }
-      int ends = 0;
-      uint32_t spins = 0;
-      uint64_t t0 = 0;
-      // keep going until every group has its END and every absmax result of
-      // this CTA is published (other CTAs' key items depend on it)
-      while (ends < NG || a_open > 0) {
-        bool any = false;
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          // retire finished stages; fold absmax results and publish layers
-          while (tail[g] < head[g]) {
-            const int k = tail[g] % NSG;
-            if (!tma::mbar_test_wait(&ctl->empty[g][k], (uint32_t)(tail[g] / NSG) & 1u)) break;
-            const Item done = ctl->items[g][k];
-            if (done.kind == kAbsmax) {
-              uint32_t m = ctl->cta_max[done.layer];
-#pragma unroll
-              for (int w = 0; w < kWarpsPerGroup; ++w) m = max(m, ctl->amax[g][k][w]);
-              ctl->cta_max[done.layer] = m;
-              --a_open;
-              if (--ctl->a_left[done.layer] == 0) {
-                __threadfence_block();
-                ctl->pub_ready[done.layer] = 1;  // the watcher publishes it
-              }
-            }
-            ++tail[g];
-            any = true;
-          }
-          if (ended[g] || head[g] - tail[g] >= NSG) continue;
-          // next item for group g: a ready key-encode item first, else absmax / value
-          Item it{kEnd, 0, 0, 0};
-          if (t_e < e_total) {
-            const int le = (int)(t_e / a.nE);
-            if (le < ctl->ready_count) {
-              it.kind = kKeyEnc;
-              it.layer = le;
-              it.idx = (int)(t_e - (long long)le * a.nE);
-              if (a.k_mode == PKV_K_TENSOR) it.pad = (int)ctl->ready_max[le];
-              t_e += G;
-            }
-          }
-          if (it.kind == kEnd && t_av < av_total) {
-            it = av_item(a, t_av);
-            t_av += G;
-          }
-          if (it.kind == kEnd && t_e < e_total) continue;  // key items wait for their layer
-          const int k = head[g] % NSG;
-          ctl->items[g][k] = it;
-          ++head[g];
-          any = true;
-          if (it.kind == kEnd) {
-            tma::mbar_arrive(&ctl->full[g][k]);
-            ended[g] = true;
-            ++ends;
-            continue;
-          }
-          uint8_t* dst = ring + (g * NSG + k) * P::STAGE;
-          uint64_t* bar = &ctl->full[g][k];
-          if (it.kind == kValEnc) {
-            tma::mbar_arrive_expect_tx(bar, (uint32_t)P::STAGE);
-            const int row0 = it.idx * TL::VR;
+      const uint64_t pol_first = tma::policy_evict_first();
+      unsigned long long t = blockIdx.x;
+      auto next_item = [&]() -> Item {
+        if (t >= a.total) return Item{kEnd, 0, 0, 0};
+        const Item it = enc_item(a, (long long)t);
+        t += gridDim.x;
+        return it;
+      };
+      auto issue = [&](const Item& it, uint8_t* dst, uint64_t* bar) {
+        if (it.kind == kValEnc) {
+          tma::mbar_arrive_expect_tx(bar, (uint32_t)P::STAGE);
+          const int row0 = it.idx * TL::VR;
 #pragma unroll 1
-            for (int rb = 0; rb < TL::NRB; ++rb)
+          for (int rb = 0; rb < TL::NRB; ++rb)
 #pragma unroll 1
-              for (int cb = 0; cb < TL::NCB; ++cb)
-                tma::tensor2d_g2s(dst + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
-                                  cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
-          } else {
-            // absmax loads keep the key chunk in L2 (evict_last) for the
-            // key-encode item that re-reads it shortly after
-            const long long e0 = (long long)it.idx * kEncChunk;
-            const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
-            tma::mbar_arrive_expect_tx(bar, bytes);
-            const TIn* src = static_cast<const TIn*>(a.k_in[it.layer]) + e0;
-            tma::bulk_g2s(dst, src, bytes, bar, it.kind == kAbsmax ? pol_last : pol_first);
-          }
+            for (int cb = 0; cb < TL::NCB; ++cb)
+              tma::tensor2d_g2s(dst + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
+                                cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
+        } else {
+          const long long e0 = (long long)it.idx * kEncChunk;
+          const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
+          tma::mbar_arrive_expect_tx(bar, bytes);
+          tma::bulk_g2s(dst, static_cast<const TIn*>(a.k_in[it.layer]) + e0, bytes, bar, pol_first);
         }
-        if (!any) {
-          __nanosleep(64);
-          tma::watchdog(spins, t0);
-        }
-      }
+      };
+      produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
     }
     return;
   }
@@ -1060,17 +954,68 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     if (it.kind == kEnd) break;
     const uint32_t in_s = tma::smem_u32(ring + (g * NSG + k) * P::STAGE);
     const bool skip = a.dbg == 1 || (a.dbg == 2 && it.kind == kValEnc) || (a.dbg == 3 && it.kind != kValEnc);
-    if (it.kind == kAbsmax) {
-      const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
-      if (lane == 0) ctl->amax[g][k][wig] = m;  // folded by the producer
-    } else if (skip) {
+    if (skip) {
     } else if (it.kind == kKeyEnc) {
-      enc_key_item<TIn>(a, it, in_s, gt, lane);
+      enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max);
     } else {
       enc_value_item<D, TIn, SYM, SIGN>(a, it, in_s, wig, lane, R, C);
     }
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);  // this warp is done with the stage
+  }
+}
+
+// ---------------------------------------------------------------------------
+// absmax kernel: max |K| bits per layer (keyquant.py:55), + non-finite flag
+// ---------------------------------------------------------------------------
+struct AbsmaxArgs {
+  int num_layers;
+  long long nelem;
+  long long chunks_per_layer;  // of kAbsChunk elements
+  const void* k_in[kMaxL];
+  unsigned int* layer_max;
+  uint32_t* status;
+};
+constexpr int kAbsThreads = 512;
+constexpr int kAbsChunk = kAbsThreads * 8 * 8;  // 8 x 16-byte loads of bf16 per thread
+
+template <typename TIn>
+__global__ void __launch_bounds__(kAbsThreads) absmax_kernel(const __grid_constant__ AbsmaxArgs a) {
+  const long long total = (long long)a.num_layers * a.chunks_per_layer;
+  __shared__ uint32_t red[kAbsThreads / 32];
+  for (long long c = blockIdx.x; c < total; c += gridDim.x) {
+    const int l = (int)(c / a.chunks_per_layer);
+    const long long e0 = (c - (long long)l * a.chunks_per_layer) * kAbsChunk;
+    const TIn* src = static_cast<const TIn*>(a.k_in[l]);
+    uint32_t m = 0;
+    constexpr int EPL = 16 / (int)sizeof(TIn);  // elements per 16-byte load
+#pragma unroll
+    for (int i = 0; i < kAbsChunk / (kAbsThreads * EPL); ++i) {
+      const long long e = e0 + ((long long)i * kAbsThreads + threadIdx.x) * EPL;
+      if (e < a.nelem) {
+        const uint4 w = ld_stream_u4(src + e);
+        if constexpr (sizeof(TIn) == 2) {
+          uint32_t h = __vmaxu2(__vmaxu2(w.x & 0x7fff7fffu, w.y & 0x7fff7fffu), __vmaxu2(w.z & 0x7fff7fffu, w.w & 0x7fff7fffu));
+          m = max(m, max(h & 0xffffu, h >> 16) << 16);
+        } else {
+          m = max(m, max(max(w.x & 0x7fffffffu, w.y & 0x7fffffffu), max(w.z & 0x7fffffffu, w.w & 0x7fffffffu)));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      m = threadIdx.x < kAbsThreads / 32 ? red[threadIdx.x] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (threadIdx.x == 0) {
+        atomicMax(a.layer_max + l, m);
+        if (m >= 0x7f800000u) atomicOr(a.status + l, PKV_FLAG_K_NONFINITE);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1313,19 +1258,17 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
   const long long vr = kEncChunk / std::max(r.head_dim, 1);
   a->nE = do_k ? (int)kch : 0;
-  a->nA = (do_k && r.k_mode == PKV_K_TENSOR) ? (int)kch : 0;
   a->nV = do_v ? (int)((r.num_vectors + vr - 1) / vr) : 0;
-  const long long total = (long long)L * (a->nA + a->nE + a->nV);
+  const long long total = (long long)L * (a->nE + a->nV);
   if (total >= (1LL << 31)) {
     delete a;
     return PKV_ERR_INVALID_ARG;
   }
-  // workspace: [u32 layer_max L][u32 layer_done L]
+  // workspace: [u32 layer_max L]
   unsigned int* w32 = reinterpret_cast<unsigned int*>(r.ws);
   a->total = (unsigned int)total;
   if (const char* dbg = std::getenv("PKV_DBG_ENC")) a->dbg = std::atoi(dbg);
   a->layer_max = w32;
-  a->layer_done = w32 + L;
   const size_t ws_need = workspace_bytes(L, r.num_vectors, r.head_dim);
   if (r.ws_bytes < ws_need) {
     delete a;
@@ -1349,9 +1292,40 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
     }
   }
   if (rc == PKV_OK && cudaMemsetAsync(r.ws, 0, ws_need, st) != cudaSuccess) rc = PKV_ERR_CUDA;
-  if (rc == PKV_OK)
-    rc = eb == 4 ? enc_launch<float>(*a, do_v ? r.head_dim : 64, r.cb.symmetric != 0, r.sign, st)
-                 : enc_launch<__nv_bfloat16>(*a, do_v ? r.head_dim : 64, r.cb.symmetric != 0, r.sign, st);
+  // Three launches, each running one code path per SM (mixing the key and
+  // value paths in one kernel thrashes the instruction cache): values, then
+  // the key absmax pass, then keys (re-reading the layers absmax touched last
+  // first, while they are still in L2).
+  const int dk = do_v ? r.head_dim : 64;
+  if (rc == PKV_OK && do_v) {
+    EncArgs* av = new EncArgs(*a);
+    av->nE = 0;
+    av->total = (unsigned int)((long long)L * av->nV);
+    rc = eb == 4 ? enc_launch<float>(*av, dk, r.cb.symmetric != 0, r.sign, st)
+                 : enc_launch<__nv_bfloat16>(*av, dk, r.cb.symmetric != 0, r.sign, st);
+    delete av;
+  }
+  if (rc == PKV_OK && do_k && r.k_mode == PKV_K_TENSOR) {
+    AbsmaxArgs m;
+    std::memset(&m, 0, sizeof(m));
+    m.num_layers = L;
+    m.nelem = nelem;
+    m.chunks_per_layer = (nelem + kAbsChunk - 1) / kAbsChunk;
+    for (int l = 0; l < L; ++l) m.k_in[l] = r.k_in[l];
+    m.layer_max = w32;
+    m.status = r.status;
+    const long long work = (long long)L * m.chunks_per_layer;
+    const int grid = (int)std::min<long long>(work, (long long)sm_count() * 4);
+    if (eb == 4) absmax_kernel<float><<<grid, kAbsThreads, 0, st>>>(m);
+    else absmax_kernel<__nv_bfloat16><<<grid, kAbsThreads, 0, st>>>(m);
+    if (cudaGetLastError() != cudaSuccess) rc = PKV_ERR_CUDA;
+  }
+  if (rc == PKV_OK && do_k) {
+    a->nV = 0;
+    a->total = (unsigned int)((long long)L * a->nE);
+    // key items never touch the value tile geometry: one instantiation serves all d
+    rc = eb == 4 ? enc_launch<float>(*a, 64, true, false, st) : enc_launch<__nv_bfloat16>(*a, 64, true, false, st);
+  }
   delete a;
   return rc;
 }
