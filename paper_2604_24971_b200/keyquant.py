@@ -47,7 +47,8 @@ class QuantizedKeyBlock:
         if tuple(codes.shape) != geometry.tensor_shape:
             raise GeometryError(
                 f"key codes shape {tuple(codes.shape)} does not match geometry {geometry.tensor_shape}")
-        device = codes.device if codes.is_cuda else _codec.require_device()
+        # trusted blocks view an existing arena (any device); user codes move to the GPU
+        device = codes.device if (codes.is_cuda or _trusted) else _codec.require_device()
         codes = codes.to(device).contiguous()
         if mode == "tensor":
             if isinstance(scale, torch.Tensor):

@@ -1,0 +1,150 @@
+"""Multi-GPU SharedKVPool: shard the write side, replicate the packed pool.
+
+SURVEY §8(e): every layer (and every KV head) of the pool is independent
+except for the per-tensor key scale, one max per layer (keyquant.py:55).
+
+* `build_pool_sharded` — each rank compresses a contiguous slice of layers
+  (no collective inside the compress), then ONE `all_gather_into_tensor` per
+  pool field over NCCL assembles the whole packed pool on every rank. The
+  gathered bytes are O(1) in agents (C4: 331.5 MB total).
+* `partition_agents` — agents are split over ranks; each rank decodes its
+  agents against its local replica, so decode needs no per-step collective.
+* `decode_attention_head_sharded` — the alternative the north star asks for
+  "where a shard boundary requires it": the pool stays sharded by KV head,
+  each rank attends over its heads and the outputs are all-gathered.
+
+Host logic here is backend-agnostic (NCCL on GPUs, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .model import KvDump, ModelGeometry
+from .pool import SharedPool, _Arena, _encode_layers, pool_from_arena, raise_for_status
+from .valuequant import GAUSSIAN_3BIT, Codebook
+
+ARENA_FIELDS = ("k_codes", "k_scale", "k_bscale", "v_packed", "v_scales", "status")
+
+
+def _world(group) -> tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def layer_shard(num_layers: int, world: int, rank: int) -> range:
+    """Contiguous, balanced slice of layers owned by `rank` (first ranks take the remainder)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    base, extra = divmod(num_layers, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def partition_agents(num_agents: int, world: int, rank: int) -> list[int]:
+    """Agent ids served by `rank` (C4: 15 agents over 8 GPUs -> 2,2,2,2,2,2,2,1)."""
+    return list(layer_shard(num_agents, world, rank))
+
+
+def _all_gather_rows(local: torch.Tensor, rows_max: int, group) -> torch.Tensor:
+    """Gather [rows_r, ...] from every rank as [world, rows_max, ...] (padded)."""
+    world, _ = _world(group)
+    padded = local
+    if local.shape[0] != rows_max:
+        padded = torch.zeros((rows_max,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        padded[:local.shape[0]] = local
+    padded = padded.contiguous()
+    if world == 1:
+        return padded.unsqueeze(0)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world * rows_max,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, padded, group=group)
+        return out.view((world, rows_max) + tuple(local.shape[1:]))
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.stack(parts)
+
+
+def gather_arena(local: _Arena, num_layers: int, group=None) -> _Arena:
+    """Assemble the full [L, ...] arena from every rank's layer slice."""
+    world, _ = _world(group)
+    rows_max = len(layer_shard(num_layers, world, 0))
+    full = object.__new__(_Arena)
+    for name in ARENA_FIELDS:
+        t = getattr(local, name, None)
+        if t is None:
+            setattr(full, name, None)
+            continue
+        g = _all_gather_rows(t, rows_max, group)
+        pieces = [g[r, :len(layer_shard(num_layers, world, r))] for r in range(world)]
+        setattr(full, name, torch.cat(pieces, dim=0).contiguous())
+    full.replay = local.replay
+    return full
+
+
+def build_pool_sharded(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_seed: int | None = None, *,
+                       k_scale_mode: str = "tensor", group=None, device=None,
+                       encode_fn: Callable | None = None) -> SharedPool:
+    """build_pool (pool.py:258-293) with the layers spread over the ranks of `group`.
+
+    Each rank reads only its own layers of `dump`; the returned pool is the
+    complete, bit-identical pool on every rank. `encode_fn` (default: the
+    sm_100a encoder) is injectable so the collective plumbing can be tested
+    on CPU ranks.
+    """
+    g: ModelGeometry = dump.geometry
+    world, rank = _world(group)
+    mine = layer_shard(g.num_layers, world, rank)
+    enc = encode_fn or _encode_layers
+    ks = [dump.layers[i][0] for i in mine]
+    vs = [dump.layers[i][1] for i in mine]
+    if ks:
+        _, _, arena = enc(ks, vs, g, codebook, sign_seed, k_scale_mode, device=device, check=False)
+    else:  # more ranks than layers: contribute an empty slice
+        arena = _Arena(g, 0, k_scale_mode, device)
+    raise_for_status(arena.status)  # data faults of this rank's layers, before the collective
+    full = gather_arena(arena, g.num_layers, group)
+    return pool_from_arena(full, g, codebook, sign_seed, k_scale_mode)
+
+
+def all_reduce_layer_max(local_max_bits: torch.Tensor, group=None) -> torch.Tensor:
+    """Per-layer max|K| across ranks when a layer's keys are split by head or
+    token: |K| bit patterns order like the floats, so a MAX
+    reduction of the int32 bit patterns is exact."""
+    world, _ = _world(group)
+    t = local_max_bits.to(torch.int32).clone()
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
+def head_shard(kv_heads: int, world: int, rank: int) -> range:
+    return layer_shard(kv_heads, world, rank)
+
+
+def decode_attention_head_sharded(attend: Callable[[torch.Tensor], torch.Tensor], q: torch.Tensor,
+                                  kv_heads: int, group=None) -> torch.Tensor:
+    """Head-sharded decode attention: rank r owns KV heads head_shard(r);
+    `attend(q_local)` runs the pool attention for those heads and returns
+    [rows, heads_r, group, d]; the result is all-gathered along the head dim.
+    q: [rows, kv_heads, group, d] (every rank holds all queries)."""
+    world, rank = _world(group)
+    hs = head_shard(kv_heads, world, rank)
+    local = attend(q[:, hs.start:hs.stop].contiguous())
+    if world == 1:
+        return local
+    hmax = len(head_shard(kv_heads, world, 0))
+    moved = local.transpose(0, 1).contiguous()  # [heads_r, rows, group, d]
+    g = _all_gather_rows(moved, hmax, group)
+    parts = [g[r, :len(head_shard(kv_heads, world, r))] for r in range(world)]
+    return torch.cat(parts, dim=0).transpose(0, 1).contiguous()
+
+
+__all__ = [
+    "ARENA_FIELDS", "all_reduce_layer_max", "build_pool_sharded", "decode_attention_head_sharded",
+    "gather_arena", "head_shard", "layer_shard", "partition_agents",
+]

@@ -126,7 +126,8 @@ class _Arena:
         self.k_bscale = (torch.empty((L, _pad(block32_count(n), 8)), dtype=torch.float16, device=device)
                          if (with_k and k_mode == "block32") else None)
         self.v_packed = torch.empty((L, _pad(packed_nbytes(n), 16)), dtype=torch.uint8, device=device) if with_v else None
-        self.v_scales = torch.empty((L, vecs), dtype=torch.float32, device=device) if with_v else None
+        # rows padded to 4 floats so every layer's scales start 16-byte aligned (TMA)
+        self.v_scales = torch.empty((L, _pad(vecs, 4)), dtype=torch.float32, device=device) if with_v else None
         self.status = torch.zeros(L, dtype=torch.int32, device=device)
         self.replay = torch.zeros(1, dtype=torch.int32, device=device)
 
@@ -205,7 +206,7 @@ def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, s
                 k_scale=[a.k_scale[i:i + 1] for i in kg] if (kg and k_scale_mode == "tensor") else None,
                 k_bscale=[a.k_bscale[i] for i in kg] if (kg and k_scale_mode == "block32") else None,
                 v_packed=[a.v_packed[i] for i in vg] if vg else None,
-                v_scales=[a.v_scales[i] for i in vg] if vg else None,
+                v_scales=[a.v_scales[i, :g.vectors_per_tensor] for i in vg] if vg else None,
                 centroids=(codebook.centroids if codebook is not None else np.zeros(8)),
                 sign_seed=sign_seed, status=status, replay=a.replay, device=device)
             if not contiguous:
@@ -214,10 +215,18 @@ def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, s
             del st
     if check:
         raise_for_status(a.status)
+    kblocks, vblocks = _blocks_from_arena(a, g, codebook, sign_seed, k_scale_mode,
+                                          [k is not None for k in ks], [v is not None for v in vs])
+    return kblocks, vblocks, a
+
+
+def _blocks_from_arena(a: "_Arena", g: ModelGeometry, codebook, sign_seed, k_scale_mode: str, has_k, has_v):
+    """Per-layer key/value blocks viewing an arena's rows (no copies)."""
+    n = g.elements_per_tensor
     kblocks, vblocks = [], []
     nb = block32_count(n)
-    for i in range(L):
-        if ks[i] is not None:
+    for i in range(len(has_k)):
+        if has_k[i]:
             kblocks.append(QuantizedKeyBlock(
                 g, a.k_scale[i:i + 1] if k_scale_mode == "tensor" else 0.0,
                 a.k_codes[i, :n].view(g.tensor_shape), mode=k_scale_mode,
@@ -225,13 +234,25 @@ def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, s
                 _trusted=True))
         else:
             kblocks.append(None)
-        if vs[i] is not None:
+        if has_v[i]:
             vblocks.append(QuantizedValueBlock(
-                g, codebook.name, codebook.bits, None, a.v_scales[i].view(g.tensor_shape[:-1]),
+                g, codebook.name, codebook.bits, None, a.v_scales[i, :g.vectors_per_tensor].view(g.tensor_shape[:-1]),
                 sign_seed, packed=a.v_packed[i, :packed_nbytes(n)], _trusted=True))
         else:
             vblocks.append(None)
-    return kblocks, vblocks, a
+    return kblocks, vblocks
+
+
+def pool_from_arena(a: "_Arena", g: ModelGeometry, codebook: Codebook = GAUSSIAN_3BIT, sign_seed=None,
+                    k_scale_mode: str = "tensor") -> "SharedPool":
+    """Seal a pool around a fully populated arena (e.g. one gathered from other GPUs)."""
+    L = g.num_layers
+    kb, vb = _blocks_from_arena(a, g, codebook, sign_seed, k_scale_mode, [True] * L, [True] * L)
+    pool = SharedPool(g, list(zip(kb, vb)), (), codebook=codebook, sign_seed=sign_seed)
+    pool._arena = a
+    pool._replay = a.replay
+    pool.status = a.status
+    return pool.seal()
 
 
 # ---------------------------------------------------------------------------

@@ -246,3 +246,16 @@ def test_decode_division_sequence_is_correctly_rounded():
     scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
     n = _lib.load().pkv_selftest(1, scratch.data_ptr(), 16, torch.cuda.current_stream().cuda_stream)
     assert n == 0, f"{n} mismatches vs IEEE division"
+
+
+def test_sharded_build_single_rank_equals_build_pool():
+    from paper_2604_24971_b200 import parallel
+
+    g = pk.ModelGeometry(num_layers=3, kv_heads=4, head_dim=128, seq_len=40)
+    dump = pk.synth_gaussian_dump(g, seed=9, device="cuda")
+    a = pk.build_pool(dump)
+    b = parallel.build_pool_sharded(dump)
+    for i in range(3):
+        (ka, va), (kb, vb) = a.layer_blocks(i), b.layer_blocks(i)
+        assert torch.equal(ka.codes, kb.codes) and ka.scale == kb.scale
+        assert torch.equal(va.packed, vb.packed) and torch.equal(va.scales, vb.scales)
