@@ -305,11 +305,10 @@ def run_ours(args, cfg):
                      torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in range(L)]
 
         def e2e_step():
-            p = pk.build_pool(host_dump, build_stats=False, device=dev)
-            view = p.attach(16)
-            for (hk, hv), (dk, dv) in zip(host_out, view.materialize_all()):
-                hk.copy_(dk, non_blocking=True)
-                hv.copy_(dv, non_blocking=True)
+            # build_pool uploads the pinned dump chunk by chunk, overlapped with
+            # the encode; materialize_to_host overlaps decode with the D2H copies
+            p = pk.build_pool(host_dump, build_stats=False, device=dev, check=False)
+            p.attach(16).materialize_to_host(host_out)
 
         e2e_step()
         torch.cuda.synchronize(dev)

@@ -353,11 +353,12 @@ class SharedPool:
         e = self.geometry.elements_per_tensor
         return (8 * e + self._layers[0][1].bits * e) * self.geometry.num_layers
 
-    def decode_layers(self, layers=None, dtype=torch.bfloat16, *, keys=True, values=True):
+    def decode_layers(self, layers=None, dtype=torch.bfloat16, *, keys=True, values=True, out=None):
         """Materialise the given layers (default: all) in ONE kernel launch.
 
         Returns a list of (K, V) tensors [B,H,T,D] of `dtype` (bf16 == the
-        reference's decode_bits=16 values; f32 == decode_bits=32).
+        reference's decode_bits=16 values; f32 == decode_bits=32). `out`: an
+        optional list of preallocated (K, V) device tensors to decode into.
         """
         g = self.geometry
         idx = list(range(self.num_layers)) if layers is None else list(layers)
@@ -365,8 +366,12 @@ class SharedPool:
             self.layer_blocks(i)
         if not idx:
             return []
-        ko = [torch.empty(g.tensor_shape, dtype=dtype, device=self.device) for _ in idx] if keys else None
-        vo = [torch.empty(g.tensor_shape, dtype=dtype, device=self.device) for _ in idx] if values else None
+        if out is not None:
+            ko = [k for k, _ in out] if keys else None
+            vo = [v for _, v in out] if values else None
+        else:
+            ko = [torch.empty(g.tensor_shape, dtype=dtype, device=self.device) for _ in idx] if keys else None
+            vo = [torch.empty(g.tensor_shape, dtype=dtype, device=self.device) for _ in idx] if values else None
         _codec.decode(
             num_vectors=g.vectors_per_tensor, head_dim=g.head_dim, out_dtype=dtype,
             k_mode=K_MODES[self.k_scale_mode],
@@ -410,6 +415,47 @@ class AgentCacheView:
         """All layers in one launch: list of (K, V) device tensors."""
         return self.pool.decode_layers(None, self.out_dtype)
 
+    def materialize_to_host(self, host_layers, chunk: int = 4) -> None:
+        """Decode every layer into caller-provided pinned host (K, V) tensors.
+
+        Layers are decoded `chunk` at a time into two alternating device
+        buffers; each chunk's device->host copy runs on a side stream while
+        the next chunk decodes. Enqueued work only: the current stream waits
+        for the last copy, so a sync of it covers everything.
+        """
+        pool, g, dt = self.pool, self.pool.geometry, self.out_dtype
+        L = pool.num_layers
+        if len(host_layers) != L:
+            raise ValueError(f"need {L} host (K, V) pairs, got {len(host_layers)}")
+        comp = torch.cuda.current_stream(pool.device)
+        copy = _side_stream(pool.device, "d2h")
+        copy.wait_stream(comp)
+        nb = min(chunk, L)
+        bufs = [[(torch.empty(g.tensor_shape, dtype=dt, device=pool.device),
+                  torch.empty(g.tensor_shape, dtype=dt, device=pool.device)) for _ in range(nb)] for _ in range(2)]
+        copied = [None, None]
+        for c, c0 in enumerate(range(0, L, chunk)):
+            idx = list(range(c0, min(L, c0 + chunk)))
+            buf = bufs[c % 2][:len(idx)]
+            if copied[c % 2] is not None:
+                comp.wait_event(copied[c % 2])  # the buffer's previous D2H has finished
+            pool.decode_layers(idx, dt, out=buf)
+            decoded = torch.cuda.Event()
+            decoded.record(comp)
+            copy.wait_event(decoded)
+            with torch.cuda.stream(copy):
+                for (hk, hv), (dk, dv) in zip((host_layers[i] for i in idx), buf):
+                    hk.copy_(dk, non_blocking=True)
+                    hv.copy_(dv, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(copy)
+            copied[c % 2] = done
+        comp.wait_stream(copy)
+        for pair in bufs:
+            for k, v in pair:
+                k.record_stream(copy)
+                v.record_stream(copy)
+
     def inject_all(self) -> InjectionTranscript:
         """Decode every layer and fingerprint what is handed over (pool.py:239-255).
 
@@ -431,18 +477,24 @@ class AgentCacheView:
 
 def build_pool(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_seed: int | None = None, *,
                k_scale_mode: str = "tensor", build_stats: str | bool = "lazy", device=None,
-               check: bool = True) -> SharedPool:
+               check: bool = True, pipeline_chunk: int = 4) -> SharedPool:
     """Quantize every layer of a dump on the GPU in one launch and seal it (pool.py:258-293).
 
     build_stats: "lazy" (default) keeps a reference to the dump and computes
     LayerStats on first access of pool.build_stats; True computes them now;
     False skips them. check=False skips the post-build status sync (call
-    raise_for_status(pool.status) later).
+    raise_for_status(pool.status) later). A dump held in pinned host memory
+    is uploaded `pipeline_chunk` layers at a time on a side stream, overlapped
+    with the encoding of the previous chunk.
     """
     g = dump.geometry
     ks = [k for k, _ in dump.layers]
     vs = [v for _, v in dump.layers]
-    kb, vb, arena = _encode_layers(ks, vs, g, codebook, sign_seed, k_scale_mode, device=device, check=check)
+    if _pinned_host(ks + vs) and g.num_layers > pipeline_chunk:
+        kb, vb, arena = _encode_from_host(ks, vs, g, codebook, sign_seed, k_scale_mode, device, check,
+                                          pipeline_chunk)
+    else:
+        kb, vb, arena = _encode_layers(ks, vs, g, codebook, sign_seed, k_scale_mode, device=device, check=check)
     pool = SharedPool(g, list(zip(kb, vb)), (), codebook=codebook, sign_seed=sign_seed)
     pool._replay = arena.replay
     pool._arena = arena
@@ -452,6 +504,51 @@ def build_pool(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_seed: int 
     elif build_stats:
         pool._build_stats = compute_layer_stats(dump, pool)
     return pool.seal()
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device, role: str = "d2h") -> torch.cuda.Stream:
+    """One upload ("h2d") and one download ("d2h") stream per device, so both
+    PCIe directions run concurrently (e.g. pool n+1 uploading while pool n's
+    decoded layers download)."""
+    key = (torch.device(device).index, role)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device)
+    return _SIDE_STREAMS[key]
+
+
+def _pinned_host(tensors) -> bool:
+    return all(t is not None and t.values.device.type == "cpu" and t.values.is_pinned() for t in tensors)
+
+
+def _encode_from_host(ks, vs, g: ModelGeometry, codebook, sign_seed, k_scale_mode, device, check, chunk):
+    """Upload chunk c+1 (side stream) while chunk c encodes (current stream)."""
+    dev = _codec.require_device(device)
+    L = len(ks)
+    arena = _Arena(g, L, k_scale_mode, dev)
+    comp = torch.cuda.current_stream(dev)
+    copy = _side_stream(dev, "h2d")  # host inputs need no device-side ordering
+    for c0 in range(0, L, chunk):
+        idx = range(c0, min(L, c0 + chunk))
+        with torch.cuda.stream(copy):
+            dk = [ks[i].values.to(dev, non_blocking=True) for i in idx]
+            dv = [vs[i].values.to(dev, non_blocking=True) for i in idx]
+            landed = torch.cuda.Event()
+            landed.record(copy)
+        comp.wait_event(landed)
+        for t in dk + dv:
+            t.record_stream(comp)
+        kc, vc = [None] * L, [None] * L
+        for j, i in enumerate(idx):
+            kc[i] = KvTensor(g, dk[j])
+            vc[i] = KvTensor(g, dv[j])
+        _encode_layers(kc, vc, g, codebook, sign_seed, k_scale_mode, device=dev, check=False, arena=arena)
+    if check:
+        raise_for_status(arena.status)
+    kb, vb = _blocks_from_arena(arena, g, codebook, sign_seed, k_scale_mode, [True] * L, [True] * L)
+    return kb, vb, arena
 
 
 def attach_agent(pool: SharedPool, decode_bits: int = 16) -> AgentCacheView:

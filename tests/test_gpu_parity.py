@@ -259,3 +259,21 @@ def test_sharded_build_single_rank_equals_build_pool():
         (ka, va), (kb, vb) = a.layer_blocks(i), b.layer_blocks(i)
         assert torch.equal(ka.codes, kb.codes) and ka.scale == kb.scale
         assert torch.equal(va.packed, vb.packed) and torch.equal(va.scales, vb.scales)
+
+
+def test_pinned_host_pipeline_equals_device_build():
+    g = pk.ModelGeometry(num_layers=7, kv_heads=4, head_dim=128, seq_len=64)
+    dump = pk.synth_gaussian_dump(g, seed=4, device="cuda", dtype=torch.bfloat16, generator="torch")
+    host = pk.KvDump(g, tuple((pk.KvTensor(g, k.values.cpu().pin_memory()), pk.KvTensor(g, v.values.cpu().pin_memory()))
+                              for k, v in dump.layers))
+    a = pk.build_pool(dump)
+    b = pk.build_pool(host, pipeline_chunk=2)
+    outs = [(torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory(),
+             torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in range(7)]
+    b.attach(16).materialize_to_host(outs, chunk=3)
+    torch.cuda.synchronize()
+    ref = a.attach(16).materialize_all()
+    for i in range(7):
+        (ka, va), (kb, vb) = a.layer_blocks(i), b.layer_blocks(i)
+        assert torch.equal(ka.codes, kb.codes) and torch.equal(va.packed, vb.packed)
+        assert torch.equal(outs[i][0], ref[i][0].cpu()) and torch.equal(outs[i][1], ref[i][1].cpu())
