@@ -53,7 +53,7 @@ constexpr int dec_groups() {
   return sizeof(TOut) == 2 ? 3 : 2;
 }
 
-enum ItemKind : int { kEnd = 0, kAbsmax = 1, kKeyEnc = 2, kValEnc = 3, kKeyDec = 4, kValDec = 5 };
+enum ItemKind : int { kEnd = 0, kAbsmax = 1, kKeyEnc = 2, kValEnc = 3, kKeyDec = 4, kValDec = 5, kBarrier = 6 };
 
 struct Item {
   int kind;
@@ -112,7 +112,10 @@ struct EncArgs {
   uint32_t sign_bits[8];
   uint32_t* status;
   uint32_t* replay_count;
-  const unsigned int* layer_max;  // [L] max |K| bits from absmax_kernel
+  unsigned int* layer_max;  // [L] max |K| bits (published by the key-role CTAs)
+  unsigned int* key_barrier;  // arrivals of key-role CTAs after their absmax phase
+  int value_ctas;             // CTAs [0, value_ctas) encode values, the rest keys
+  int nA;                     // absmax items per layer (per-tensor mode)
   const void* k_in[kMaxL];
   const void* v_in[kMaxL];
   int8_t* k_codes[kMaxL];
@@ -149,6 +152,12 @@ __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned lon
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// arithmetic shift right by 31 (all ones for a set sign bit), kept as one SHF
+__device__ __forceinline__ uint32_t sar31(uint32_t x) {
+  uint32_t r;
+  asm("shr.s32 %0, %1, 31;" : "=r"(r) : "r"(x));
+  return r;
+}
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, f2(-1.f, -1.f), a); }
 
@@ -171,11 +180,13 @@ __device__ __forceinline__ void fwht_pairs(float2* xp) {
       xp[p + h] = sub2(a, b);
     }
   }
-  // coordinate bit 3: inside each pair, (x, y) -> (x + y, x - y)
+  // coordinate bit 3: inside each pair, (x, y) -> (x + y, x - y). Two scalar
+  // ops: a paired FFMA2 would need a (1, -1) register pair per use.
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    const float2 a = xp[p];
-    xp[p] = __ffma2_rn(f2(1.f, -1.f), f2(a.y, a.y), f2(a.x, a.x));
+    const float a = xp[p].x, b = xp[p].y;
+    xp[p].x = a + b;
+    xp[p].y = a - b;
   }
   // coordinate bits 4.. : pair-index bits 3..
 #pragma unroll
@@ -416,14 +427,14 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         gb = fminf(gb, fminf(fabsf(d2.x), fabsf(d2.y)));
         ga = fminf(ga, fminf(fabsf(d3.x), fabsf(d3.y)));
         gb = fminf(gb, fminf(au.x, au.y));
-        // mm = #thresholds above |u|; code = negative ? mm : 7 - mm
+        // mm = #thresholds above |u|; code = negative ? mm : 7 - mm = (mm ^ 7 ^ sign) & 7
         const uint32_t mx = (__float_as_uint(d1.x) >> 31) + (__float_as_uint(d2.x) >> 31) + (__float_as_uint(d3.x) >> 31);
         const uint32_t my = (__float_as_uint(d1.y) >> 31) + (__float_as_uint(d2.y) >> 31) + (__float_as_uint(d3.y) >> 31);
-        const uint32_t cx = (mx ^ ~(uint32_t)((int32_t)__float_as_uint(u.x) >> 31)) & 7u;
-        const uint32_t cy = (my ^ ~(uint32_t)((int32_t)__float_as_uint(u.y) >> 31)) & 7u;
+        const uint32_t cx = (mx ^ 7u ^ sar31(__float_as_uint(u.x))) & 7u;
+        const uint32_t cy = (my ^ 7u ^ sar31(__float_as_uint(u.y))) & 7u;
         const int c0 = (p >> 3) * 2, e = p & 7;
-        words[c0] |= cx << (3 * e);
-        words[c0 + 1] |= cy << (3 * e);
+        words[c0] += cx << (3 * e);  // disjoint fields: + == |, one LEA
+        words[c0 + 1] += cy << (3 * e);
       }
       const float g = fminf(fminf(gacc[0], gacc[1]), fminf(gacc[2], gacc[3]));
       replay |= g < DL;
@@ -495,10 +506,16 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   uint32_t m = 0;
-#pragma unroll 4
-  for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
-    const int u = i * kGroupThreads + gt;
-    if (u * 8 < n) m = max(m, lds_absmax8<TIn>(in_s + u * 8 * (int)sizeof(TIn)));
+  if (n == kEncChunk) {
+#pragma unroll
+    for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i)
+      m = max(m, lds_absmax8<TIn>(in_s + (i * kGroupThreads + gt) * 8 * (int)sizeof(TIn)));
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
+      const int u = i * kGroupThreads + gt;
+      if (u * 8 < n) m = max(m, lds_absmax8<TIn>(in_s + u * 8 * (int)sizeof(TIn)));
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -525,16 +542,21 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     // half-point are re-coded exactly afterwards (rare)
     constexpr int ITERS = kEncChunk / 8 / kGroupThreads;
     uint32_t need = 0;
-#pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
+    auto chunk = [&](int i) {
       const int u = i * kGroupThreads + gt;
-      if (u * 8 < n) {
-        float x[8];
-        lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
-        bool bad;
-        st_u2(dst + u * 8, key_chunk_fast(x, make_float2(rcp, rcp), bad));
-        need |= (uint32_t)bad << i;
-      }
+      float x[8];
+      lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
+      bool bad;
+      st_u2(dst + u * 8, key_chunk_fast(x, make_float2(rcp, rcp), bad));
+      need |= (uint32_t)bad << i;
+    };
+    if (n == kEncChunk) {  // full item: straight-line code, chunks interleave
+#pragma unroll
+      for (int i = 0; i < ITERS; ++i) chunk(i);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < ITERS; ++i)
+        if ((i * kGroupThreads + gt) * 8 < n) chunk(i);
     }
     if (exact_all) need = (1u << ITERS) - 1u;
 #pragma unroll 1
@@ -600,10 +622,11 @@ __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, ui
   const float ts = tensor ? __ldg(a.k_scale[it.layer]) : 0.f;
   const __half* bsc = a.k_bscale[it.layer];
   const uint32_t out_s = tma::smem_u32(out);
-#pragma unroll 4
+  const bool full = n == kDecChunk;
+#pragma unroll
   for (int i = 0; i < kDecChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
-    if (u * 8 >= n) continue;
+    if (!full && u * 8 >= n) continue;
     const uint2 w = tma::lds64(in_s + u * 8);
     const float s = tensor ? ts : __half2float(__ldg(bsc + ((e0 + u * 8) >> 5)));
     const uint32_t wx = w.x ^ 0x80808080u, wy = w.y ^ 0x80808080u;
@@ -674,9 +697,9 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
   const float* gsc = a.v_scales[it.layer] + vbase;
   const float* ssc = reinterpret_cast<const float*>(in + 3 * kDecChunk / 8);
   const uint32_t out_s = tma::smem_u32(out);
-  const float2 c2 = f2(a.sqrt_d32, a.sqrt_d32), r2 = f2(a.rcp_sqrt_d32, a.rcp_sqrt_d32);
-  char* tb = reinterpret_cast<char*>(tbl);
-  const uint32_t lane_off = (uint32_t)gt * 4u;
+  const float2 nc2 = f2(-a.sqrt_d32, -a.sqrt_d32), r2 = f2(a.rcp_sqrt_d32, a.rcp_sqrt_d32);
+  // table[code][gt] at tbl_s | code << 9 | gt << 2  (tables are 4 KB aligned)
+  const uint32_t lane_off = tma::smem_u32(tbl) + (uint32_t)gt * 4u;
 #pragma unroll 1
   for (int pass = 0; pass < TL::PASSES; ++pass) {
     const int vr = pass * TL::PER_PASS + wig * G::VPW + r;
@@ -701,10 +724,10 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
     for (int c = 0; c < NCL; ++c) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        // byte address (code << 9) | lane_off   (kGroupThreads * 4 == 512)
+        // shared address lane_off | (code << 9)   (kGroupThreads * 4 == 512)
         const int sh = 3 * e;
         const uint32_t off = (sh <= 9 ? (words[c] << (9 - sh)) : (words[c] >> (sh - 9))) & 0xe00u;
-        const float val = *reinterpret_cast<const float*>(tb + (off | lane_off));
+        const float val = __uint_as_float(tma::lds32(off | lane_off));
         if (c & 1) xp[(c >> 1) * 8 + e].y = val;
         else xp[(c >> 1) * 8 + e].x = val;
       }
@@ -721,7 +744,7 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
         if (pow4) {
           xp[p] = q;
         } else {
-          const float2 e = __ffma2_rn(f2(-q.x, -q.y), c2, xp[p]);
+          const float2 e = __ffma2_rn(q, nc2, xp[p]);  // x - q*c, exact remainder
           xp[p] = __ffma2_rn(e, r2, q);
         }
       }
@@ -753,24 +776,24 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
 // ---------------------------------------------------------------------------
 // ticket -> item
 // ---------------------------------------------------------------------------
-// Encode work list: layers in reverse order; per layer the value items
-// V(l, *) interleaved with the key items E(l, *). CTA b takes items b, b + G,
-// b + 2G, ... (items are independent).
-__device__ __forceinline__ Item enc_item(const EncArgs& a, long long t) {
-  const long long per = (long long)a.nE + a.nV;
-  Item it{kEnd, 0, 0, 0};
+// Encode work lists. The grid is split by role (one code path per SM):
+//   value CTAs [0, value_ctas):  V(l, j) for all layers, layer-major;
+//   key CTAs:   A(l, j) for all layers (per-tensor mode), a key-role barrier,
+//               then E(l, j) with layers in REVERSE order, so the layers the
+//               absmax phase read last are still L2-resident.
+// Each CTA walks a static round-robin slice of its role's list.
+__device__ __forceinline__ Item enc_value_item_at(const EncArgs& a, long long t) {
+  Item it{kValEnc, 0, 0, 0};
+  it.layer = (int)(t / a.nV);
+  it.idx = (int)(t - (long long)it.layer * a.nV);
+  return it;
+}
+__device__ __forceinline__ Item enc_key_item_at(const EncArgs& a, long long t, bool absmax) {
+  Item it{absmax ? kAbsmax : kKeyEnc, 0, 0, 0};
+  const int per = absmax ? a.nA : a.nE;
   const int r = (int)(t / per);
-  it.layer = a.num_layers - 1 - r;
-  long long off = t - (long long)r * per;
-  const long long both = 2 * (long long)min(a.nE, a.nV);
-  if (off < both) {
-    it.kind = (off & 1) ? kKeyEnc : kValEnc;
-    it.idx = (int)(off >> 1);
-  } else {
-    off -= both;
-    it.kind = a.nE > a.nV ? kKeyEnc : kValEnc;
-    it.idx = (int)(min(a.nE, a.nV) + off);
-  }
+  it.layer = absmax ? r : a.num_layers - 1 - r;
+  it.idx = (int)(t - (long long)r * per);
   return it;
 }
 
@@ -823,7 +846,8 @@ struct alignas(8) Ctl {
   uint64_t full[kMaxGroups][kMaxSG];
   uint64_t empty[kMaxGroups][kMaxSG];
   Item items[kMaxGroups][kMaxSG];
-  uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer (absmax_kernel ran before)
+  uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer, staged after the key barrier
+  uint32_t amax[kMaxL];       // encode: this CTA's absmax fold (shared atomics)
 };
 
 template <int D, typename TIn>
@@ -834,7 +858,7 @@ constexpr size_t enc_smem_bytes() {
 template <typename TOut>
 constexpr size_t dec_smem_bytes() {
   using P = DecPlan<(int)sizeof(TOut), dec_groups<TOut>()>;
-  return 1024 + (size_t)P::OUT_TOTAL + (size_t)P::NG * P::NSG * P::STAGE + sizeof(Ctl) +
+  return 4096 + (size_t)P::OUT_TOTAL + (size_t)P::NG * P::NSG * P::STAGE + sizeof(Ctl) +
          (size_t)P::NG * 8 * kGroupThreads * sizeof(float);
 }
 
@@ -848,6 +872,15 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // bar) starts its TMA loads.
 template <int NG, int NSG, class Next, class Issue>
 __device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes, Next next_item, Issue issue) {
+  produce<NG, NSG>(ctl, ring, stage_bytes, next_item, issue, [] {});
+}
+
+// As above; an item of kind kBarrier is not issued: the producer waits until
+// every stage issued so far has been released by its consumers, then runs
+// on_barrier() and continues with the following items.
+template <int NG, int NSG, class Next, class Issue, class Barrier>
+__device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes, Next next_item, Issue issue,
+                                        Barrier on_barrier) {
   int head[NG];
   bool ended[NG];
 #pragma unroll
@@ -865,7 +898,18 @@ __device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes
       if (ended[g]) continue;
       const int k = head[g] % NSG, use = head[g] / NSG;
       if (use >= 1 && !tma::mbar_test_wait(&ctl->empty[g][k], (uint32_t)(use - 1) & 1u)) continue;
-      const Item it = next_item();
+      Item it = next_item();
+      if (it.kind == kBarrier) {
+        // drain: the last use of every stage of every group has been released
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg)
+          for (int kk = 0; kk < NSG; ++kk) {
+            const int uses = head[gg] / NSG + (kk < head[gg] % NSG ? 1 : 0);
+            if (uses >= 1) tma::mbar_wait(&ctl->empty[gg][kk], (uint32_t)(uses - 1) & 1u);
+          }
+        on_barrier();
+        it = next_item();
+      }
       ctl->items[g][k] = it;
       ++head[g];
       any = true;
@@ -905,20 +949,14 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       }
     tma::fence_mbar_init();
   }
-  if (threadIdx.x < a.num_layers && a.layer_max) ctl->layer_max[threadIdx.x] = __ldg(a.layer_max + threadIdx.x);
+  if (threadIdx.x < kMaxL) ctl->amax[threadIdx.x] = 0;
   __syncthreads();
+  const bool value_role = (int)blockIdx.x < a.value_ctas;
 
   if (warp == 0) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      const uint64_t pol_first = tma::policy_evict_first();
-      unsigned long long t = blockIdx.x;
-      auto next_item = [&]() -> Item {
-        if (t >= a.total) return Item{kEnd, 0, 0, 0};
-        const Item it = enc_item(a, (long long)t);
-        t += gridDim.x;
-        return it;
-      };
+      const uint64_t pol_first = tma::policy_evict_first(), pol_last = tma::policy_evict_last();
       auto issue = [&](const Item& it, uint8_t* dst, uint64_t* bar) {
         if (it.kind == kValEnc) {
           tma::mbar_arrive_expect_tx(bar, (uint32_t)P::STAGE);
@@ -930,13 +968,68 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
               tma::tensor2d_g2s(dst + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
                                 cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
         } else {
+          // absmax reads keep the keys in L2 for the key-encode phase
           const long long e0 = (long long)it.idx * kEncChunk;
           const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
           tma::mbar_arrive_expect_tx(bar, bytes);
-          tma::bulk_g2s(dst, static_cast<const TIn*>(a.k_in[it.layer]) + e0, bytes, bar, pol_first);
+          tma::bulk_g2s(dst, static_cast<const TIn*>(a.k_in[it.layer]) + e0, bytes, bar,
+                        it.kind == kAbsmax ? pol_last : pol_first);
         }
       };
-      produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
+      if (value_role) {
+        const long long G = a.value_ctas, total = (long long)a.num_layers * a.nV;
+        long long t = blockIdx.x;
+        auto next_item = [&]() -> Item {
+          if (t >= total) return Item{kEnd, 0, 0, 0};
+          const Item it = enc_value_item_at(a, t);
+          t += G;
+          return it;
+        };
+        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
+      } else {
+        const long long G = (long long)gridDim.x - a.value_ctas;
+        const long long b = (long long)blockIdx.x - a.value_ctas;
+        const long long ta = (long long)a.num_layers * a.nA, te = (long long)a.num_layers * a.nE;
+        long long t = b;
+        int phase = a.nA > 0 ? 0 : 2;  // 0 absmax, 1 barrier pending, 2 key encode
+        auto next_item = [&]() -> Item {
+          if (phase == 0) {
+            if (t < ta) {
+              const Item it = enc_key_item_at(a, t, true);
+              t += G;
+              return it;
+            }
+            phase = 1;
+            t = b;
+            return Item{kBarrier, 0, 0, 0};
+          }
+          phase = 2;
+          if (t >= te) return Item{kEnd, 0, 0, 0};
+          const Item it = enc_key_item_at(a, t, false);
+          t += G;
+          return it;
+        };
+        auto barrier = [&]() {
+          // every absmax item of this CTA is folded into ctl->amax: publish,
+          // then wait for all key CTAs and stage the layer maxima
+          for (int l = 0; l < a.num_layers; ++l) {
+            const uint32_t m = ctl->amax[l];
+            if (m) atomicMax(a.layer_max + l, m);
+          }
+          __threadfence();
+          atomicAdd(a.key_barrier, 1u);
+          uint32_t spins = 0;
+          uint64_t t0 = 0;
+          while (*reinterpret_cast<volatile const uint32_t*>(a.key_barrier) < (uint32_t)G) {
+            __nanosleep(256);
+            tma::watchdog(spins, t0);
+          }
+          __threadfence();
+          for (int l = 0; l < a.num_layers; ++l)
+            ctl->layer_max[l] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + l);
+        };
+        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue, barrier);
+      }
     }
     return;
   }
@@ -954,7 +1047,10 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     if (it.kind == kEnd) break;
     const uint32_t in_s = tma::smem_u32(ring + (g * NSG + k) * P::STAGE);
     const bool skip = a.dbg == 1 || (a.dbg == 2 && it.kind == kValEnc) || (a.dbg == 3 && it.kind != kValEnc);
-    if (skip) {
+    if (it.kind == kAbsmax) {
+      const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
+      if (lane == 0) atomicMax(&ctl->amax[it.layer], m);  // folded per CTA, published at the key barrier
+    } else if (skip) {
     } else if (it.kind == kKeyEnc) {
       enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max);
     } else {
@@ -1029,9 +1125,11 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
   constexpr int NG = P::NG, NSG = P::NSG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* obuf = align1024(smem_raw);  // 1024-aligned swizzled output tiles
-  uint8_t* ring = obuf + P::OUT_TOTAL;
+  uint8_t* base4k = smem_raw + ((4096u - (tma::smem_u32(smem_raw) & 4095u)) & 4095u);
+  obuf = base4k;                         // 4 KB aligned (>= the 1 KB swizzle alignment)
+  float* tables = reinterpret_cast<float*>(obuf + P::OUT_TOTAL);  // 4 KB aligned per group
+  uint8_t* ring = obuf + P::OUT_TOTAL + P::NG * 8 * kGroupThreads * sizeof(float);
   Ctl* ctl = reinterpret_cast<Ctl*>(ring + NG * NSG * P::STAGE);
-  float* tables = reinterpret_cast<float*>(ctl + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int g = 0; g < NG; ++g)
@@ -1174,7 +1272,8 @@ int coop_launch(K kernel, const void* args, size_t smem, int threads, cudaStream
     return PKV_ERR_CUDA;
   void* params[] = {const_cast<void*>(args)};
   const cudaError_t e =
-      cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)(sm_count() * per_sm)), dim3(threads), params,
+      // one persistent CTA per SM (the role split and static slices assume it)
+      cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)sm_count()), dim3(threads), params,
                                   smem, st);
   return e == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
@@ -1292,39 +1391,26 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
     }
   }
   if (rc == PKV_OK && cudaMemsetAsync(r.ws, 0, ws_need, st) != cudaSuccess) rc = PKV_ERR_CUDA;
-  // Three launches, each running one code path per SM (mixing the key and
-  // value paths in one kernel thrashes the instruction cache): values, then
-  // the key absmax pass, then keys (re-reading the layers absmax touched last
-  // first, while they are still in L2).
-  const int dk = do_v ? r.head_dim : 64;
-  if (rc == PKV_OK && do_v) {
-    EncArgs* av = new EncArgs(*a);
-    av->nE = 0;
-    av->total = (unsigned int)((long long)L * av->nV);
-    rc = eb == 4 ? enc_launch<float>(*av, dk, r.cb.symmetric != 0, r.sign, st)
-                 : enc_launch<__nv_bfloat16>(*av, dk, r.cb.symmetric != 0, r.sign, st);
-    delete av;
-  }
-  if (rc == PKV_OK && do_k && r.k_mode == PKV_K_TENSOR) {
-    AbsmaxArgs m;
-    std::memset(&m, 0, sizeof(m));
-    m.num_layers = L;
-    m.nelem = nelem;
-    m.chunks_per_layer = (nelem + kAbsChunk - 1) / kAbsChunk;
-    for (int l = 0; l < L; ++l) m.k_in[l] = r.k_in[l];
-    m.layer_max = w32;
-    m.status = r.status;
-    const long long work = (long long)L * m.chunks_per_layer;
-    const int grid = (int)std::min<long long>(work, (long long)sm_count() * 4);
-    if (eb == 4) absmax_kernel<float><<<grid, kAbsThreads, 0, st>>>(m);
-    else absmax_kernel<__nv_bfloat16><<<grid, kAbsThreads, 0, st>>>(m);
-    if (cudaGetLastError() != cudaSuccess) rc = PKV_ERR_CUDA;
-  }
-  if (rc == PKV_OK && do_k) {
-    a->nV = 0;
-    a->total = (unsigned int)((long long)L * a->nE);
-    // key items never touch the value tile geometry: one instantiation serves all d
-    rc = eb == 4 ? enc_launch<float>(*a, 64, true, false, st) : enc_launch<__nv_bfloat16>(*a, 64, true, false, st);
+  // One launch; the grid is split by role so every SM runs a single code
+  // path (mixing the key and value paths on one SM thrashes its instruction
+  // cache): value CTAs are ALU-bound, key CTAs (absmax pass, key barrier,
+  // key encode) are HBM-bound, and the two overlap.
+  const int dk = do_v ? r.head_dim : 64;  // key-only launches never touch the value tile geometry
+  if (rc == PKV_OK) {
+    a->nA = (do_k && r.k_mode == PKV_K_TENSOR) ? a->nE : 0;
+    a->key_barrier = w32 + L;
+    const int grid = sm_count();  // one CTA per SM (checked by the launcher)
+    int key_ctas = 0;
+    if (do_k && do_v) {
+      double frac = 0.2;  // share of SMs for the key role (C3-tuned; PKV_KEY_SM_FRACTION overrides)
+      if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
+      key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
+    } else if (do_k) {
+      key_ctas = grid;
+    }
+    a->value_ctas = grid - key_ctas;
+    rc = eb == 4 ? enc_launch<float>(*a, dk, r.cb.symmetric != 0, r.sign, st)
+                 : enc_launch<__nv_bfloat16>(*a, dk, r.cb.symmetric != 0, r.sign, st);
   }
   delete a;
   return rc;
