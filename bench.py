@@ -53,28 +53,51 @@ def algorithmic_bytes(L, H, D, T, in_bytes, out_bytes, k_mode="tensor"):
 # clocks
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled every ~5 ms during the timed
+    region (NVML via nvidia-ml-py; falls back to nvidia-smi)."""
+
+    # NVML clocks-event reason bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+            self.max_mhz = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            p = self._nvml
+            sm = p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)
+            try:
+                r = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                r = p.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            return sm, [n for bit, n in self.REASONS.items() if r & bit]
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        sm, mx = (float(x) for x in out.strip().split(",")[:2])
+        self.max_mhz = mx
+        return sm, []
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                parts = [p.strip() for p in out.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.005)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -87,13 +110,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({r for _, rs in self.samples for r in rs})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -402,8 +423,8 @@ def run_ours(args, cfg):
                         "encode_values_ms": enc_v_ms, "encode_values_gbs": bytes_v / (enc_v_ms / 1e3) / 1e9,
                         "encode_keys_ms": enc_k_ms, "encode_keys_gbs": bytes_k / (enc_k_ms / 1e3) / 1e9,
                         "encode_bytes": comp_b, "decode_bytes": deq_b, "cuda_graph": graphed},
-            # per step: value-encode, key-absmax, key-encode, decode (+ one memset)
-            "gpu_launches": (4 if args.k_mode == "tensor" else 3) * args.steps,
+            # per step: one encode launch (value + key roles) and one decode launch (+ one memset)
+            "gpu_launches": 2 * args.steps,
             "clocks": clocks.summary(),
             "e2e": e2e,
             "decode_attention": attn,

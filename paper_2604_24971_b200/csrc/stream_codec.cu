@@ -18,10 +18,11 @@
 //     / writes its 16-byte chunks without bank conflicts.
 //
 // Per-tensor key scales (keyquant.py:55) need max|K| over a whole layer
-// before any key code can be written. A short absmax pass over all layers
-// (absmax_kernel) runs first; the encode kernel then walks the layers in
-// REVERSE order so the key tensors the absmax pass touched last are still
-// L2-resident when they are re-read.
+// before any key code can be written. The encode grid is split by role: value
+// CTAs stream V (ALU-bound), key CTAs run an absmax pass over every layer
+// (L2 evict_last), meet at a key-role barrier, then encode the keys walking
+// the layers in REVERSE order so the layers read last are still in L2. Each
+// SM runs a single code path (mixing both on one SM thrashes its I-cache).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -529,7 +530,7 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
   if (a.k_mode == PKV_K_TENSOR) {
-    const uint32_t pb = layer_max[it.layer];  // from absmax_kernel (stream-ordered), staged in smem
+    const uint32_t pb = layer_max[it.layer];  // published at the key-role barrier, staged in smem
     const bool nonfinite = pb >= 0x7f800000u;
     const float s = (nonfinite || pb == 0) ? 0.f : __uint_as_float(pb) / 127.0f;  // f32(peak/127), keyquant.py:60
     if (it.idx == 0 && gt == 0) {
@@ -1062,60 +1063,6 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
-// absmax kernel: max |K| bits per layer (keyquant.py:55), + non-finite flag
-// ---------------------------------------------------------------------------
-struct AbsmaxArgs {
-  int num_layers;
-  long long nelem;
-  long long chunks_per_layer;  // of kAbsChunk elements
-  const void* k_in[kMaxL];
-  unsigned int* layer_max;
-  uint32_t* status;
-};
-constexpr int kAbsThreads = 512;
-constexpr int kAbsChunk = kAbsThreads * 8 * 8;  // 8 x 16-byte loads of bf16 per thread
-
-template <typename TIn>
-__global__ void __launch_bounds__(kAbsThreads) absmax_kernel(const __grid_constant__ AbsmaxArgs a) {
-  const long long total = (long long)a.num_layers * a.chunks_per_layer;
-  __shared__ uint32_t red[kAbsThreads / 32];
-  for (long long c = blockIdx.x; c < total; c += gridDim.x) {
-    const int l = (int)(c / a.chunks_per_layer);
-    const long long e0 = (c - (long long)l * a.chunks_per_layer) * kAbsChunk;
-    const TIn* src = static_cast<const TIn*>(a.k_in[l]);
-    uint32_t m = 0;
-    constexpr int EPL = 16 / (int)sizeof(TIn);  // elements per 16-byte load
-#pragma unroll
-    for (int i = 0; i < kAbsChunk / (kAbsThreads * EPL); ++i) {
-      const long long e = e0 + ((long long)i * kAbsThreads + threadIdx.x) * EPL;
-      if (e < a.nelem) {
-        const uint4 w = ld_stream_u4(src + e);
-        if constexpr (sizeof(TIn) == 2) {
-          uint32_t h = __vmaxu2(__vmaxu2(w.x & 0x7fff7fffu, w.y & 0x7fff7fffu), __vmaxu2(w.z & 0x7fff7fffu, w.w & 0x7fff7fffu));
-          m = max(m, max(h & 0xffffu, h >> 16) << 16);
-        } else {
-          m = max(m, max(max(w.x & 0x7fffffffu, w.y & 0x7fffffffu), max(w.z & 0x7fffffffu, w.w & 0x7fffffffu)));
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      m = threadIdx.x < kAbsThreads / 32 ? red[threadIdx.x] : 0u;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (threadIdx.x == 0) {
-        atomicMax(a.layer_max + l, m);
-        if (m >= 0x7f800000u) atomicOr(a.status + l, PKV_FLAG_K_NONFINITE);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
 // decode kernel
 // ---------------------------------------------------------------------------
 template <int D, typename TOut, bool SIGN>
@@ -1329,7 +1276,7 @@ size_t workspace_bytes(int num_layers, long long num_vectors, int head_dim) {
   const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
   const long long L = std::min(std::max(num_layers, 0), kMaxL);
   (void)kch;
-  return (size_t)(L * 8 + 16);
+  return (size_t)(L * 8 + 16);  // [u32 layer_max L][u32 layer_done L / key barrier]
 }
 
 int encode(const EncodeRequest& r, cudaStream_t st) {
@@ -1402,7 +1349,9 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
     const int grid = sm_count();  // one CTA per SM (checked by the launcher)
     int key_ctas = 0;
     if (do_k && do_v) {
-      double frac = 0.2;  // share of SMs for the key role (C3-tuned; PKV_KEY_SM_FRACTION overrides)
+      // share of SMs for the key role (swept on C3 bf16: 0.3 -> 328 us, 0.4 -> 296 us,
+      // 0.5 -> 341 us); PKV_KEY_SM_FRACTION overrides
+      double frac = 0.4;
       if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
       key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
     } else if (do_k) {
