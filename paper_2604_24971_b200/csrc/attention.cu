@@ -9,11 +9,12 @@
 // Layout of the work:
 //   * all agents' query rows that share a KV head (rows = agents * group) are
 //     processed together, so each pool tile is read from HBM once per step;
-//   * the prefix is split into 128-token tiles, one CTA per (kv head, tile);
-//     a CTA converts its K tile (int8 codes * scale, exactly the reference
-//     dequant) to f32 in shared memory and its V tile to the *rotated*
-//     domain y = table[code] * rms (valuequant.py:232-234), then computes
-//     scores, a tile-local softmax (max, sum) and sum_t p_t * y_t;
+//   * the prefix is cut into ~2 splits per SM, one CTA per (kv head, split,
+//     64-row tile); a CTA walks its split in 64-token tiles, converting each
+//     K tile (int8 codes * scale, exactly the reference dequant) to f32 in
+//     shared memory and each V tile to the *rotated* domain
+//     y = table[code] * rms (valuequant.py:232-234), and runs register-tiled
+//     fp32 S = Q K / P Y products with an online (flash) softmax;
 //   * a combine kernel merges the tiles with log-sum-exp weights, applies
 //     ONE inverse FWHT / sqrt(d) (and the sign diagonal) per output vector —
 //     valid because H is linear — and folds in the agent's private bf16
@@ -28,9 +29,6 @@
 namespace pkv {
 namespace attn {
 
-constexpr int TT = 128;        // prefix tokens per CTA
-constexpr int RT = 64;         // query rows per row tile (8 warps x 8 rows)
-constexpr int kAttnThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Args {
@@ -53,7 +51,7 @@ struct Args {
   const void* tail_v;
   const int32_t* tail_len;
   int tail_cap;
-  float* part;     // [kv_heads][splits][rows][D + 2]
+  float* part;     // [kv_heads][splits][rows][D + 4]: acc[D], m, l, pad (16 B rows)
   void* out;
 };
 
@@ -62,178 +60,248 @@ __device__ __forceinline__ float ldq(const Args& a, long long i) {
                               : __bfloat162float(static_cast<const __nv_bfloat16*>(a.q)[i]);
 }
 
-// smem: Kt[D][TT] f32 | Y[TT][D] f32 | Q[RT][D] f32 | P[RT][TT] f32
-template <int D>
-__global__ void __launch_bounds__(kAttnThreads, 1) prefix_kernel(const __grid_constant__ Args a) {
-  extern __shared__ __align__(16) float sm[];
-  float* Kt = sm;
-  float* Y = Kt + D * TT;
-  float* Q = Y + TT * D;
-  float* P = Q + RT * D;
+// ---------------------------------------------------------------------------
+// prefix kernel: register-tiled fp32 attention over one split of the prefix
+// ---------------------------------------------------------------------------
+// CTA = (kv head h, split sp, row tile). The split covers a contiguous token
+// range, walked in tiles of TT2 tokens with an online (flash) softmax, so
+// partials are written once per split. Per tile:
+//   Ks[d][t]  = k code * key scale (dequantize_k, keyquant.py:71), f32
+//   Ys[t][d]  = table[code] * rms  (rotated-domain V, valuequant.py:232-234)
+//   S = Q Ks (16 x 16 threads, TR rows x 4 tokens each), P = exp2(S - m)
+//   O += P Ys (16 x 16 threads, TR rows x D/16 columns each)
+// The pool's per-tensor key scale and log2(e)*softmax_scale are applied in
+// fp32 exactly like the reference path: s = (q * qscale) . k_deq.
+constexpr int TT2 = 64;
+constexpr int kAttnThreads2 = 256;
+
+template <int D, int RT>
+struct AttnTile {
+  static constexpr int TR = RT / 16;       // rows per thread
+  static constexpr int TD = D / 16;        // output columns per thread
+  static constexpr int Q_FLOATS = D * RT;  // Qs[d][r]
+  static constexpr int K_FLOATS = D * TT2; // Ks[d][t]
+  static constexpr int P_FLOATS = TT2 * RT;// Ps[t][r]
+  static constexpr int Y_FLOATS = TT2 * D; // Ys[t][d]
+  static_assert(P_FLOATS <= K_FLOATS, "P overlays the consumed K tile");
+  // raw (packed) tile staged by cp.async while the previous tile computes
+  static constexpr int RAW_K = TT2 * D;            // int8 codes
+  static constexpr int RAW_V = TT2 * 3 * D / 8;    // packed values
+  static constexpr int RAW_S = TT2 * 4;            // f32 scales
+  static constexpr int RAW = RAW_K + RAW_V + RAW_S;
+  static constexpr size_t SMEM = sizeof(float) * (size_t)(Q_FLOATS + K_FLOATS + Y_FLOATS) + RAW;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void lds_vec(const float* p, float (&v)[N]) {
+  if constexpr (N == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (N == 8) {
+    const float4 t0 = *reinterpret_cast<const float4*>(p), t1 = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = t0.x; v[1] = t0.y; v[2] = t0.z; v[3] = t0.w; v[4] = t1.x; v[5] = t1.y; v[6] = t1.z; v[7] = t1.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = p[i];
+  }
+}
+
+template <int D, int RT>
+__global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_constant__ Args a) {
+  using AT = AttnTile<D, RT>;
+  constexpr int TR = AT::TR, TD = AT::TD;
+  extern __shared__ __align__(16) float sm2[];
+  float* Qs = sm2;
+  float* Ks = Qs + AT::Q_FLOATS;
+  float* Ps = Ks;  // P overlays K once S = Q K is done
+  float* Ys = Ks + AT::K_FLOATS;
   __shared__ float cent[8];
 
   const int h = blockIdx.y;
-  const int sidx = blockIdx.x;
-  const long long t0 = (long long)sidx * TT;
-  const int nt = (int)min((long long)TT, a.T - t0);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sp = blockIdx.x;
+  const int r0 = blockIdx.z * RT;
+  const long long per = (a.T + a.splits - 1) / a.splits;
+  const long long t_begin = (long long)sp * per, t_end = min(a.T, t_begin + per);
+  const int tid = threadIdx.x;
+  const int rg = tid >> 4, cg = tid & 15;  // row group, column (token / d) group
   if (tid < 8) cent[tid] = a.cent32[tid];
-  __syncthreads();
 
-  // ---- K tile -> f32, transposed (Kt[d][t]) ----
-  {
-    const int t = tid % TT;
-    const long long tok = t0 + t;
-    for (int d0 = (tid / TT) * 16; d0 < D; d0 += (kAttnThreads / TT) * 16) {
+  // ---- Q row tile, pre-scaled by softmax_scale * log2(e): Qs[d][r] ----
+  // (8 consecutive d per thread: one 16-byte load for bf16 queries)
+  for (int i = tid; i < RT * D / 8; i += kAttnThreads2) {
+    const int r = i / (D / 8), d0 = (i % (D / 8)) * 8;
+    const int row = r0 + r;
+    float qv[8];
+    if (row < a.rows) {
+      const int agent = row / a.group, g = row % a.group;
+      const long long off = (((long long)agent * a.kv_heads + h) * a.group + g) * D + d0;
+      if (a.q_dtype == PKV_BF16) {
+        const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + off);
+        qv[0] = bf16lo(w.x); qv[1] = bf16hi(w.x); qv[2] = bf16lo(w.y); qv[3] = bf16hi(w.y);
+        qv[4] = bf16lo(w.z); qv[5] = bf16hi(w.z); qv[6] = bf16lo(w.w); qv[7] = bf16hi(w.w);
+      } else {
+        const float4 x0 = *reinterpret_cast<const float4*>(static_cast<const float*>(a.q) + off);
+        const float4 x1 = *reinterpret_cast<const float4*>(static_cast<const float*>(a.q) + off + 4);
+        qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w; qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qv[j] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) Qs[(d0 + j) * RT + r] = qv[j] * a.qscale;
+  }
+
+  float m_run[TR], l_run[TR], acc[TR][TD];
+#pragma unroll
+  for (int i = 0; i < TR; ++i) {
+    m_run[i] = -INFINITY;
+    l_run[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < TD; ++j) acc[i][j] = 0.f;
+  }
+  const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 0.f;
+
+  uint8_t* raw = reinterpret_cast<uint8_t*>(Ys + AT::Y_FLOATS);
+  int8_t* rk = reinterpret_cast<int8_t*>(raw);
+  uint8_t* rv = raw + AT::RAW_K;
+  float* rs = reinterpret_cast<float*>(raw + AT::RAW_K + AT::RAW_V);
+  // stage the packed tile [t0, t0 + nt) of head h into raw shared memory
+  auto stage = [&](long long t0, int nt) {
+    const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
+    for (int i = tid; i < nt * D / 16; i += kAttnThreads2) cp_async16(rk + i * 16, gk + i * 16);
+    const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
+    for (int i = tid; i < nt * (3 * D / 8) / 4; i += kAttnThreads2) cp_async4(rv + i * 4, gv + i * 4);
+    const float* gs = a.v_scales + (long long)h * a.T + t0;
+    for (int i = tid; i < nt; i += kAttnThreads2) cp_async4(rs + i, gs + i);
+    cp_async_commit();
+  };
+  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT2, t_end - t_begin));
+
+  for (long long t0 = t_begin; t0 < t_end; t0 += TT2) {
+    const int nt = (int)min((long long)TT2, t_end - t0);
+    cp_async_wait_all();
+    __syncthreads();  // raw tile landed; previous tile's Ks / Ys / Ps are consumed
+    // ---- K tile -> Ks[d][t] (f32 dequant); 8 lanes read one token's 128 B ----
+    for (int i = tid; i < TT2 * (D / 16); i += kAttnThreads2) {
+      const int t = i / (D / 16), d0 = (i % (D / 16)) * 16;
       float kv[16];
       if (t < nt) {
-        const long long base = ((long long)h * a.T + tok) * D + d0;
-        const uint4 w = *reinterpret_cast<const uint4*>(a.k_codes + base);
+        const uint4 w = *reinterpret_cast<const uint4*>(rk + t * D + d0);
         const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        const float s = a.k_mode == PKV_K_TENSOR ? ts
+                                                 : __half2float(a.k_bscale[(((long long)h * a.T + t0 + t) * D + d0) >> 5]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = (int)(int8_t)((ww[j >> 2] >> (8 * (j & 3))) & 0xffu);
-          const float s = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale)
-                                                   : __half2float(a.k_bscale[(base + j) >> 5]);
-          kv[j] = (float)c * s;  // dequantize_k: code * scale in f32
-        }
+        for (int j = 0; j < 16; ++j) kv[j] = (float)(int)(int8_t)((ww[j >> 2] >> (8 * (j & 3))) & 0xffu) * s;
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) kv[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) Kt[(d0 + j) * TT + t] = kv[j];
+      for (int j = 0; j < 16; ++j) Ks[(d0 + j) * TT2 + t] = kv[j];
     }
-  }
-  // ---- V tile -> rotated-domain values Y[t][d] = table[code] * rms ----
-  {
-    constexpr int W = D / 8;
-    for (int i = tid; i < TT * W; i += kAttnThreads) {
-      const int t = i / W, w = i % W;
+    // ---- V tile -> Ys[t][d] = table[code] * rms ----
+    for (int i = tid; i < TT2 * (D / 8); i += kAttnThreads2) {
+      const int t = i / (D / 8), w8 = i % (D / 8);
       float y[8];
       if (t < nt) {
-        const long long v = (long long)h * a.T + t0 + t;
-        const uint8_t* p = a.v_packed + v * (3 * D / 8) + 3 * w;
+        const uint8_t* p = rv + t * (3 * D / 8) + 3 * w8;
         const uint32_t word = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
-        const float rms = a.v_scales[v];
+        const float rms = rs[t];
 #pragma unroll
         for (int e = 0; e < 8; ++e) y[e] = cent[(word >> (3 * e)) & 7u] * rms;
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) y[e] = 0.f;
       }
-      float4* dst = reinterpret_cast<float4*>(Y + t * D + 8 * w);
+      float4* dst = reinterpret_cast<float4*>(Ys + t * D + 8 * w8);
       dst[0] = make_float4(y[0], y[1], y[2], y[3]);
       dst[1] = make_float4(y[4], y[5], y[6], y[7]);
     }
-  }
+    __syncthreads();  // raw buffer free: prefetch the next tile while this one computes
+    if (t0 + TT2 < t_end) stage(t0 + TT2, (int)min((long long)TT2, t_end - t0 - TT2));
 
-  constexpr int DPL = D / 32;  // output columns per lane in the PV product
-  for (int r0 = 0; r0 < a.rows; r0 += RT) {
-    __syncthreads();
-    // ---- Q row tile (pre-scaled by softmax_scale * log2 e) ----
-    for (int i = tid; i < RT * D; i += kAttnThreads) {
-      const int r = i / D, d = i % D;
-      const int row = r0 + r;
-      float qv = 0.f;
-      if (row < a.rows) {
-        const int agent = row / a.group, g = row % a.group;
-        qv = ldq(a, (((long long)agent * a.kv_heads + h) * a.group + g) * D + d) * a.qscale;
-      }
-      Q[r * D + d] = qv;
+    // ---- S = Q K: thread (rg, cg) -> rows rg*TR.., tokens cg*4.. ----
+    float sc[TR][4];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sc[i][j] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < D; ++d) {
+      float qa[TR], kb[4];
+      lds_vec<TR>(Qs + d * RT + rg * TR, qa);
+      lds_vec<4>(Ks + d * TT2 + cg * 4, kb);
+#pragma unroll
+      for (int i = 0; i < TR; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sc[i][j] = fmaf(qa[i], kb[j], sc[i][j]);
     }
-    __syncthreads();
-
-    // ---- scores: warp -> 8 rows, lane -> 4 tokens ----
-    float s[8][4];
+    __syncthreads();  // every thread is done reading Ks (P overwrites it)
+    // ---- online softmax over this tile (16 threads share a row group) ----
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s[i][j] = 0.f;
-    const float* qrow = Q + (warp * 8) * D;
-#pragma unroll 2
-    for (int d = 0; d < D; d += 4) {
-      float4 kk[4];
-#pragma unroll
-      for (int dd = 0; dd < 4; ++dd) kk[dd] = *reinterpret_cast<const float4*>(Kt + (d + dd) * TT + 4 * lane);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 qq = *reinterpret_cast<const float4*>(qrow + i * D + d);
-        s[i][0] = fmaf(qq.x, kk[0].x, s[i][0]); s[i][1] = fmaf(qq.x, kk[0].y, s[i][1]);
-        s[i][2] = fmaf(qq.x, kk[0].z, s[i][2]); s[i][3] = fmaf(qq.x, kk[0].w, s[i][3]);
-        s[i][0] = fmaf(qq.y, kk[1].x, s[i][0]); s[i][1] = fmaf(qq.y, kk[1].y, s[i][1]);
-        s[i][2] = fmaf(qq.y, kk[1].z, s[i][2]); s[i][3] = fmaf(qq.y, kk[1].w, s[i][3]);
-        s[i][0] = fmaf(qq.z, kk[2].x, s[i][0]); s[i][1] = fmaf(qq.z, kk[2].y, s[i][1]);
-        s[i][2] = fmaf(qq.z, kk[2].z, s[i][2]); s[i][3] = fmaf(qq.z, kk[2].w, s[i][3]);
-        s[i][0] = fmaf(qq.w, kk[3].x, s[i][0]); s[i][1] = fmaf(qq.w, kk[3].y, s[i][1]);
-        s[i][2] = fmaf(qq.w, kk[3].z, s[i][2]); s[i][3] = fmaf(qq.w, kk[3].w, s[i][3]);
-      }
-    }
-    // ---- tile softmax: row max, p = 2^(s - m), row sum ----
-    float mrow[8], lrow[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < TR; ++i) {
       float m = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (4 * lane + j >= nt) s[i][j] = -INFINITY;
-        m = fmaxf(m, s[i][j]);
+        if (cg * 4 + j >= nt) sc[i][j] = -INFINITY;
+        m = fmaxf(m, sc[i][j]);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      const float m_new = fmaxf(m_run[i], m);
+      const float corr = exp2f(m_run[i] - m_new);  // 0 on the first tile
       float l = 0.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float p = exp2f(s[i][j] - m);
-        s[i][j] = p;
+        const float p = exp2f(sc[i][j] - m_new);
+        sc[i][j] = p;
         l += p;
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-      mrow[i] = m;
-      lrow[i] = l;
-      *reinterpret_cast<float4*>(P + (warp * 8 + i) * TT + 4 * lane) =
-          make_float4(s[i][0], s[i][1], s[i][2], s[i][3]);
+      for (int o = 8; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      l_run[i] = l_run[i] * corr + l;
+      m_run[i] = m_new;
+#pragma unroll
+      for (int j = 0; j < TD; ++j) acc[i][j] *= corr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Ps[(cg * 4 + j) * RT + rg * TR + i] = sc[i][j];
     }
-    __syncwarp();  // each warp only reads back its own P rows
-
-    // ---- PV in the rotated domain: warp -> 8 rows, lane -> DPL columns ----
-    float acc[8][DPL];
+    __syncthreads();
+    // ---- O += P Y: thread (rg, cg) -> rows rg*TR.., columns cg*TD.. ----
+#pragma unroll 4
+    for (int t = 0; t < TT2; ++t) {
+      float pa[TR], yb[TD];
+      lds_vec<TR>(Ps + t * RT + rg * TR, pa);
+      lds_vec<TD>(Ys + t * D + cg * TD, yb);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TR; ++i)
 #pragma unroll
-      for (int j = 0; j < DPL; ++j) acc[i][j] = 0.f;
-    const float* prow = P + (warp * 8) * TT;
-    for (int t = 0; t < nt; t += 4) {
-      float yv[4][DPL];
-#pragma unroll
-      for (int tt = 0; tt < 4; ++tt)
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) yv[tt][j] = Y[(t + tt) * D + lane * DPL + j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 pp = *reinterpret_cast<const float4*>(prow + i * TT + t);
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-          acc[i][j] = fmaf(pp.x, yv[0][j], acc[i][j]);
-          acc[i][j] = fmaf(pp.y, yv[1][j], acc[i][j]);
-          acc[i][j] = fmaf(pp.z, yv[2][j], acc[i][j]);
-          acc[i][j] = fmaf(pp.w, yv[3][j], acc[i][j]);
-        }
-      }
+        for (int j = 0; j < TD; ++j) acc[i][j] = fmaf(pa[i], yb[j], acc[i][j]);
     }
-    // ---- partial: [h][split][row][0..D) acc, D: m, D+1: l ----
+  }
+  // ---- partial: [h][split][row][0..D) acc, D: m, D+1: l ----
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = r0 + warp * 8 + i;
-      if (row >= a.rows) continue;
-      float* dst = a.part + (((long long)h * a.splits + sidx) * a.rows + row) * (D + 2);
+  for (int i = 0; i < TR; ++i) {
+    const int row = r0 + rg * TR + i;
+    if (row >= a.rows) continue;
+    float* dst = a.part + (((long long)h * a.splits + sp) * a.rows + row) * (D + 4);
 #pragma unroll
-      for (int j = 0; j < DPL; ++j) dst[lane * DPL + j] = acc[i][j];
-      if (lane == 0) {
-        dst[D] = mrow[i];
-        dst[D + 1] = lrow[i];
-      }
+    for (int j = 0; j < TD; ++j) dst[cg * TD + j] = acc[i][j];
+    if (cg == 0) {
+      dst[D] = m_run[i];
+      dst[D + 1] = l_run[i];
     }
   }
 }
@@ -249,21 +317,32 @@ __global__ void combine_kernel(const __grid_constant__ Args a) {
   const int h = warp_global % a.kv_heads;
   const int agent = row / a.group, g = row % a.group;
 
+  const long long stride = (long long)a.rows * (D + 4);  // between splits
+  const float* base = a.part + ((long long)h * a.splits * a.rows + row) * (D + 4);
+  // split maxima: lanes in parallel over splits
   float M = -INFINITY;
-  for (int sidx = 0; sidx < a.splits; ++sidx) {
-    const float* src = a.part + (((long long)h * a.splits + sidx) * a.rows + row) * (D + 2);
-    M = fmaxf(M, src[D]);
-  }
+  for (int sidx = lane; sidx < a.splits; sidx += 32) M = fmaxf(M, base[sidx * stride + D]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float L = 0.f;
   float acc[EPL];
 #pragma unroll
   for (int j = 0; j < EPL; ++j) acc[j] = 0.f;
+#pragma unroll 4
   for (int sidx = 0; sidx < a.splits; ++sidx) {
-    const float* src = a.part + (((long long)h * a.splits + sidx) * a.rows + row) * (D + 2);
+    const float* src = base + sidx * stride;
     const float w = exp2f(src[D] - M);
     L += w * src[D + 1];
+    float v[EPL];
+    if constexpr (EPL == 4) {
+      const float4 t = *reinterpret_cast<const float4*>(src + 4 * lane);
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
 #pragma unroll
-    for (int j = 0; j < EPL; ++j) acc[j] = fmaf(w, src[EPL * lane + j], acc[j]);
+      for (int j = 0; j < EPL; ++j) v[j] = src[EPL * lane + j];
+    }
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) acc[j] = fmaf(w, v[j], acc[j]);
   }
   // inverse rotation of the merged rotated-domain accumulator:
   // in-lane stages over the low log2(EPL) bits, shuffles over the lane bits
@@ -332,23 +411,35 @@ __global__ void combine_kernel(const __grid_constant__ Args a) {
   }
 }
 
-template <int D>
-size_t smem_bytes() {
-  return sizeof(float) * (size_t)(D * TT + TT * D + RT * D + RT * TT);
+// splits per head: about two CTAs per SM (two co-resident CTAs hide each
+// other's tile loads), each split at least one tile
+inline int attn_splits(int kv_heads, long long T, int row_tiles) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = (2LL * sms + (long long)kv_heads * row_tiles - 1) / ((long long)kv_heads * row_tiles);
+  const long long max_splits = (T + TT2 - 1) / TT2;
+  return (int)std::max(1LL, std::min(want, max_splits));
 }
 
-template <int D>
-int launch(Args& a, cudaStream_t st) {
-  const size_t smem = smem_bytes<D>();
-  if (cudaFuncSetAttribute(prefix_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem) != cudaSuccess)
+template <int D, int RTILE>
+int launch_rt(Args& a, cudaStream_t st) {
+  using AT = AttnTile<D, RTILE>;
+  if (cudaFuncSetAttribute(prefix_kernel2<D, RTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)AT::SMEM) != cudaSuccess)
     return PKV_ERR_CUDA;
-  dim3 grid(a.splits, a.kv_heads);
-  prefix_kernel<D><<<grid, kAttnThreads, smem, st>>>(a);
+  const int row_tiles = (a.rows + RTILE - 1) / RTILE;
+  dim3 grid(a.splits, a.kv_heads, row_tiles);
+  prefix_kernel2<D, RTILE><<<grid, kAttnThreads2, AT::SMEM, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
   const int warps = a.rows * a.kv_heads;
   combine_kernel<D><<<(warps + 7) / 8, 256, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+}
+
+template <int D>
+int launch(Args& a, cudaStream_t st) {
+  return a.rows <= 16 ? launch_rt<D, 16>(a, st) : launch_rt<D, 64>(a, st);
 }
 
 }  // namespace attn
@@ -359,9 +450,9 @@ extern "C" {
 size_t pkv_attention_workspace_bytes(int num_rows, int kv_heads, int group, int head_dim,
                                      int64_t seq_len) {
   if (num_rows < 1 || kv_heads < 1 || group < 1 || head_dim < 1 || seq_len < 1) return 0;
-  const long long splits = (seq_len + pkv::attn::TT - 1) / pkv::attn::TT;
-  return sizeof(float) * (size_t)kv_heads * (size_t)splits * (size_t)num_rows * (size_t)group *
-         (size_t)(head_dim + 2);
+  const int rows = num_rows * group;
+  const int splits = pkv::attn::attn_splits(kv_heads, seq_len, (rows + (rows <= 16 ? 15 : 63)) / (rows <= 16 ? 16 : 64));
+  return sizeof(float) * (size_t)kv_heads * (size_t)splits * (size_t)rows * (size_t)(head_dim + 4);
 }
 
 int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, int64_t seq_len,
@@ -397,7 +488,10 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, in
   a.q_dtype = q_dtype;
   a.out_dtype = out_dtype;
   a.k_mode = k_mode;
-  a.splits = (int)((seq_len + TT - 1) / TT);
+  {
+    const int rt = a.rows <= 16 ? 16 : 64;
+    a.splits = attn_splits(kv_heads, seq_len, (a.rows + rt - 1) / rt);
+  }
   a.qscale = softmax_scale * kLog2e;
   for (int i = 0; i < 8; ++i) a.cent32[i] = (float)centroids_host[i];
   if (sign_bits_host) {
