@@ -373,6 +373,20 @@ def run_ours(args, cfg):
                 "agents": agents, "layers": L, "scope": "attention only (all layers), batched agents",
                 "pool_gbs": pool_bytes / (a_ms / 1e3) / 1e9}
 
+    # ---- model-level shared-pool decode (random-init model of the config's shape) ----
+    dec_e2e = None
+    if not args.skip_decode_e2e and args.config in ("c2", "c3") and rank == 0:
+        try:
+            sys.path.insert(0, str(ROOT / "tools"))
+            import decode_bench
+
+            dec_e2e = decode_bench.run(args.config, steps=32)
+            dec_e2e["scope"] = ("greedy decode, agents in lockstep, random-init model; pooled = PooledCache + "
+                                "pkv_decode_attention, materialized = per-agent bf16 DynamicCache + SDPA "
+                                "(reference semantics) on the same GPU")
+        except Exception as exc:  # noqa: BLE001
+            dec_e2e = {"error": repr(exc)[:300]}
+
     peak, peak_kind = measured_peaks()
     n = g.elements_per_tensor
     vecs = g.vectors_per_tensor
@@ -428,6 +442,7 @@ def run_ours(args, cfg):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "decode_attention": attn,
+            "decode_e2e": dec_e2e,
             "replayed_vectors_per_build": pool.replay_count,
             "cpu_baseline": cpu,
         }
@@ -450,6 +465,7 @@ def main():
     ap.add_argument("--skip-attention", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graphs")
+    ap.add_argument("--skip-decode-e2e", action="store_true", help="skip the model-level decode measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -142,7 +142,8 @@ class PooledLayer(CacheLayerMixin):
         self.capacity = max(1, tail_capacity)
         self.decode_bits = decode_bits
         self.tail_len = 0
-        self._len_t: torch.Tensor | None = None
+        self._len_t: torch.Tensor | None = None  # device tail length (read by the attention kernel)
+        self._pos_t: torch.Tensor | None = None  # device write position of the next token
 
     @property
     def prefix_len(self) -> int:
@@ -154,6 +155,7 @@ class PooledLayer(CacheLayerMixin):
         self.keys = torch.zeros((B, H, self.capacity, D), dtype=torch.bfloat16, device=self.device)
         self.values = torch.zeros_like(self.keys)
         self._len_t = torch.zeros(B, dtype=torch.int32, device=self.device)
+        self._pos_t = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.is_initialized = True
 
     def _grow(self, need: int) -> None:
@@ -172,17 +174,35 @@ class PooledLayer(CacheLayerMixin):
         if not self.is_initialized:
             self.lazy_initialization(key_states, value_states)
         n = key_states.shape[-2]
-        self._grow(self.tail_len + n)
-        self.keys[:, :, self.tail_len:self.tail_len + n] = key_states.to(torch.bfloat16)
-        self.values[:, :, self.tail_len:self.tail_len + n] = value_states.to(torch.bfloat16)
-        self.tail_len += n
-        self._len_t.fill_(self.tail_len)
+        if n == 1:
+            # decode step: device-side position, so the step can be CUDA-graph
+            # captured and replayed (no Python int baked into the launches)
+            if self.tail_len + 1 > self.capacity:
+                self._grow(self.tail_len + 1)
+            self.keys.index_copy_(2, self._pos_t, key_states.to(torch.bfloat16))
+            self.values.index_copy_(2, self._pos_t, value_states.to(torch.bfloat16))
+            self._len_t.add_(1)
+            self._pos_t.add_(1)
+            self.tail_len += 1
+            k, v = self.keys, self.values  # full buffers: the kernel reads _len_t
+        else:
+            self._grow(self.tail_len + n)
+            self.keys[:, :, self.tail_len:self.tail_len + n] = key_states.to(torch.bfloat16)
+            self.values[:, :, self.tail_len:self.tail_len + n] = value_states.to(torch.bfloat16)
+            self.tail_len += n
+            self._len_t.fill_(self.tail_len)
+            self._pos_t.fill_(self.tail_len)
+            k = self.keys[:, :, :self.tail_len]
+            v = self.values[:, :, :self.tail_len]
         # the attention function recognises pooled layers by this marker
-        k = self.keys[:, :, :self.tail_len]
-        v = self.values[:, :, :self.tail_len]
         k._pkv_layer = (self, n)
         v._pkv_layer = (self, n)
         return k, v
+
+    def sync_lengths(self) -> None:
+        """Re-read the tail length from the device (after CUDA-graph replays)."""
+        if self._len_t is not None:
+            self.tail_len = int(self._len_t[0].item())
 
     def get_mask_sizes(self, query_length: int) -> tuple[int, int]:
         return self.prefix_len + self.tail_len + query_length, 0
@@ -220,6 +240,10 @@ class PooledCache(Cache):
         super().__init__(layers=layers)
         self.pool = pool
         self.batch = batch
+
+    def sync_lengths(self) -> None:
+        for layer in self.layers:
+            layer.sync_lengths()
 
 
 def pooled_attention_forward(module, query: torch.Tensor, key: torch.Tensor, value: torch.Tensor,
