@@ -624,12 +624,19 @@ __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, ui
   const __half* bsc = a.k_bscale[it.layer];
   const uint32_t out_s = tma::smem_u32(out);
   const bool full = n == kDecChunk;
+  const int sm_scales = ((((n + 31) / 32) * 2) & ~15) / 2;  // block scales staged in smem
 #pragma unroll
   for (int i = 0; i < kDecChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
     if (!full && u * 8 >= n) continue;
     const uint2 w = tma::lds64(in_s + u * 8);
-    const float s = tensor ? ts : __half2float(__ldg(bsc + ((e0 + u * 8) >> 5)));
+    float s = ts;
+    if (!tensor) {
+      const int b = (u * 8) >> 5;
+      s = b < sm_scales ? __half2float(__ushort_as_half((unsigned short)(tma::lds32(in_s + kDecChunk + (b & ~1) * 2) >>
+                                                                          (16 * (b & 1)))))
+                        : __half2float(__ldg(bsc + ((e0 + u * 8) >> 5)));
+    }
     const uint32_t wx = w.x ^ 0x80808080u, wy = w.y ^ 0x80808080u;
     float y[8];
 #pragma unroll
@@ -835,7 +842,7 @@ struct EncPlan {
 template <int EB_OUT, int NG_>
 struct DecPlan {
   static constexpr int NG = NG_;
-  static constexpr int STAGE = kDecChunk;  // >= key codes, packed values + scales
+  static constexpr int STAGE = kDecChunk + 1024;  // key codes + block32 scales / packed values + scales
   static constexpr int OUT = kDecChunk * EB_OUT;
   static constexpr int NOB = 2;            // output buffers per group
   static constexpr int OUT_TOTAL = NG * NOB * OUT;
@@ -1104,8 +1111,12 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
         if (it.kind == kKeyDec) {
           const long long e0 = (long long)it.idx * kDecChunk;
           const uint32_t bytes = (uint32_t)min((long long)kDecChunk, a.nelem - e0);
-          tma::mbar_arrive_expect_tx(bar, bytes);
+          // block32: the item's fp16 scales follow the codes (whole 16-byte units;
+          // a ragged last unit is read from global memory by the consumer)
+          const uint32_t sb = a.k_mode == PKV_K_TENSOR ? 0u : ((bytes + 31) / 32 * 2) & ~15u;
+          tma::mbar_arrive_expect_tx(bar, bytes + sb);
           tma::bulk_g2s(in, a.k_codes[it.layer] + e0, bytes, bar, pol_first);
+          if (sb) tma::bulk_g2s(in + kDecChunk, a.k_bscale[it.layer] + (e0 >> 5), sb, bar, pol_first);
         } else {
           const long long v0 = (long long)it.idx * TL::VR;
           const int nv = (int)min((long long)TL::VR, a.nvec - v0);
