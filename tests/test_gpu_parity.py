@@ -277,3 +277,40 @@ def test_pinned_host_pipeline_equals_device_build():
         (ka, va), (kb, vb) = a.layer_blocks(i), b.layer_blocks(i)
         assert torch.equal(ka.codes, kb.codes) and torch.equal(va.packed, vb.packed)
         assert torch.equal(outs[i][0], ref[i][0].cpu()) and torch.equal(outs[i][1], ref[i][1].cpu())
+
+
+def test_verify_passes_and_catches_a_flipped_byte():
+    # kvpool verify (cli.py:216-315); test_cli.py:64-73 flips one payload byte
+    from paper_2604_24971_b200.verify import verify_pool
+
+    g = pk.ModelGeometry(num_layers=3, kv_heads=4, head_dim=64, seq_len=96)
+    dump = pk.synth_gaussian_dump(g, seed=12, device="cuda")
+    pool = pk.build_pool(dump)
+    rep = verify_pool(dump, pool, agents=(1, 4))
+    assert rep.ok, rep.lines()
+    pool.layer_blocks(1)[1].packed[7] ^= 0x10
+    rep = verify_pool(dump, pool, agents=(1, 2))
+    assert not rep.ok and "payload" in [line for line in rep.lines() if line.startswith("FAIL")][0]
+
+
+def test_config2_shape_sampled_layers_bit_exact():
+    # BASELINE configs[1]: SmolLM2 shape at 1,851 tokens; three layers checked
+    L, H, D, T = 24, 32, 64, 1851
+    g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
+    layers = O.synth_dump(L, H, D, T, seed=0)
+    dump = pk.KvDump(g, tuple((pk.KvTensor(g, torch.from_numpy(k).cuda().to(torch.bfloat16)),
+                               pk.KvTensor(g, torch.from_numpy(v).cuda().to(torch.bfloat16))) for k, v in layers))
+    pool = pk.build_pool(dump, build_stats=False)
+    dec = pool.attach(16).materialize_all()
+    for li in (0, 11, 23):
+        k = dump.layers[li][0].values.float().cpu().numpy()
+        v = dump.layers[li][1].values.float().cpu().numpy()
+        scale, kc = O.quantize_k_tensor(k)
+        vc, vs = O.quantize_v(v)
+        kq, vq = pool.layer_blocks(li)
+        assert kq.scale == scale and np.array_equal(kq.codes.cpu().numpy(), kc)
+        assert np.array_equal(vq.codes.cpu().numpy(), vc)
+        assert np.array_equal(u32(vq.scales), vs.view(np.uint32))
+        kd, vd = O.decode_layer(kc, scale, vc, vs, 16)
+        assert np.array_equal(u32(dec[li][0]), kd.view(np.uint32))
+        assert np.array_equal(u32(dec[li][1]), vd.view(np.uint32))
