@@ -163,13 +163,14 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
     for (int j = 0; j < 8; ++j) Qs[(d0 + j) * RT + r] = qv[j] * a.qscale;
   }
 
-  float m_run[TR], l_run[TR], acc[TR][TD];
+  float m_run[TR], l_run[TR];
+  float2 acc[TR][TD / 2];  // column pairs, updated with FFMA2
 #pragma unroll
   for (int i = 0; i < TR; ++i) {
     m_run[i] = -INFINITY;
     l_run[i] = 0.f;
 #pragma unroll
-    for (int j = 0; j < TD; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TD / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
   }
   const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 0.f;
 
@@ -233,20 +234,26 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
     if (t0 + TT2 < t_end) stage(t0 + TT2, (int)min((long long)TT2, t_end - t0 - TT2));
 
     // ---- S = Q K: thread (rg, cg) -> rows rg*TR.., tokens cg*4.. ----
-    float sc[TR][4];
+    // paired fp32 FMAs (FFMA2): token pairs (k_j, k_j+1) x broadcast q_i
+    float2 sc2[TR][2];
 #pragma unroll
-    for (int i = 0; i < TR; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sc[i][j] = 0.f;
+    for (int i = 0; i < TR; ++i) sc2[i][0] = sc2[i][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int d = 0; d < D; ++d) {
-      float qa[TR], kb[4];
+      float qa[TR];
       lds_vec<TR>(Qs + d * RT + rg * TR, qa);
-      lds_vec<4>(Ks + d * TT2 + cg * 4, kb);
+      const float4 kb = *reinterpret_cast<const float4*>(Ks + d * TT2 + cg * 4);
+      const float2 k01 = make_float2(kb.x, kb.y), k23 = make_float2(kb.z, kb.w);
 #pragma unroll
-      for (int i = 0; i < TR; ++i)
+      for (int i = 0; i < TR; ++i) {
+        sc2[i][0] = __ffma2_rn(make_float2(qa[i], qa[i]), k01, sc2[i][0]);
+        sc2[i][1] = __ffma2_rn(make_float2(qa[i], qa[i]), k23, sc2[i][1]);
+      }
+    }
+    float sc[TR][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sc[i][j] = fmaf(qa[i], kb[j], sc[i][j]);
+    for (int i = 0; i < TR; ++i) {
+      sc[i][0] = sc2[i][0].x; sc[i][1] = sc2[i][0].y; sc[i][2] = sc2[i][1].x; sc[i][3] = sc2[i][1].y;
     }
     __syncthreads();  // every thread is done reading Ks (P overwrites it)
     // ---- online softmax over this tile (16 threads share a row group) ----
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
       l_run[i] = l_run[i] * corr + l;
       m_run[i] = m_new;
 #pragma unroll
-      for (int j = 0; j < TD; ++j) acc[i][j] *= corr;
+      for (int j = 0; j < TD / 2; ++j) acc[i][j] = __fmul2_rn(acc[i][j], make_float2(corr, corr));
 #pragma unroll
       for (int j = 0; j < 4; ++j) Ps[(cg * 4 + j) * RT + rg * TR + i] = sc[i][j];
     }
@@ -288,7 +295,8 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
 #pragma unroll
       for (int i = 0; i < TR; ++i)
 #pragma unroll
-        for (int j = 0; j < TD; ++j) acc[i][j] = fmaf(pa[i], yb[j], acc[i][j]);
+        for (int j = 0; j < TD / 2; ++j)
+          acc[i][j] = __ffma2_rn(make_float2(pa[i], pa[i]), make_float2(yb[2 * j], yb[2 * j + 1]), acc[i][j]);
     }
   }
   // ---- partial: [h][split][row][0..D) acc, D: m, D+1: l ----
@@ -298,7 +306,10 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
     if (row >= a.rows) continue;
     float* dst = a.part + (((long long)h * a.splits + sp) * a.rows + row) * (D + 4);
 #pragma unroll
-    for (int j = 0; j < TD; ++j) dst[cg * TD + j] = acc[i][j];
+    for (int j = 0; j < TD / 2; ++j) {
+      dst[cg * TD + 2 * j] = acc[i][j].x;
+      dst[cg * TD + 2 * j + 1] = acc[i][j].y;
+    }
     if (cg == 0) {
       dst[D] = m_run[i];
       dst[D + 1] = l_run[i];

@@ -314,3 +314,43 @@ def test_config2_shape_sampled_layers_bit_exact():
         kd, vd = O.decode_layer(kc, scale, vc, vs, 16)
         assert np.array_equal(u32(dec[li][0]), kd.view(np.uint32))
         assert np.array_equal(u32(dec[li][1]), vd.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_shapes_tails_and_modes_bit_exact(seed):
+    """Ragged shapes through the TMA paths: token counts that leave partial
+    tiles / partial bulk copies, every supported head_dim, bf16 and f32 inputs,
+    both key modes, sign diagonals; everything bit-exact vs the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    D = int(rng.choice([16, 32, 64, 128]))
+    H = int(rng.integers(1, 5))
+    T = int(rng.integers(1, 700))
+    L = int(rng.integers(1, 4))
+    dtype = torch.bfloat16 if seed % 2 else torch.float32
+    mode = "block32" if seed % 3 == 2 else "tensor"
+    sign_seed = 7 if seed % 3 == 1 else None
+    g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
+    layers = O.synth_dump(L, H, D, T, seed=seed)
+    dump = pk.KvDump(g, tuple((pk.KvTensor(g, torch.from_numpy(k).cuda().to(dtype)),
+                               pk.KvTensor(g, torch.from_numpy(v).cuda().to(dtype))) for k, v in layers))
+    pool = pk.build_pool(dump, sign_seed=sign_seed, k_scale_mode=mode, build_stats=False)
+    for bits in (16, 32):
+        dec = pool.attach(bits).materialize_all()
+        for li in range(L):
+            k = dump.layers[li][0].values.float().cpu().numpy()
+            v = dump.layers[li][1].values.float().cpu().numpy()
+            vc, vs = O.quantize_v(v, sign_seed=sign_seed)
+            kq, vq = pool.layer_blocks(li)
+            if mode == "tensor":
+                scale, kc = O.quantize_k_tensor(k)
+                assert kq.scale == scale
+                kd, vd = O.decode_layer(kc, scale, vc, vs, bits, sign_seed=sign_seed)
+            else:
+                s16, kc = O.quantize_k_block32(k)
+                assert np.array_equal(kq.block_scales.cpu().numpy().view(np.uint16), s16.view(np.uint16))
+                kd, vd = O.decode_layer(kc, 0.0, vc, vs, bits, sign_seed=sign_seed, k_block_scales=s16)
+            assert np.array_equal(kq.codes.cpu().numpy(), kc), (li, D, T)
+            assert np.array_equal(vq.codes.cpu().numpy(), vc), (li, D, T)
+            assert np.array_equal(u32(vq.scales), vs.view(np.uint32))
+            assert np.array_equal(u32(dec[li][0]), kd.view(np.uint32)), (li, bits)
+            assert np.array_equal(u32(dec[li][1]), vd.view(np.uint32)), (li, bits)
