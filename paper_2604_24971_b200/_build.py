@@ -56,15 +56,25 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     """Compile every csrc/*.cu and *.cpp into lib/libpolykv.so."""
     if not force and not _stale():
         return LIB_PATH
-    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    return _compile(LIB_PATH, LIB_DIR / "obj", [], verbose)
+
+
+def build_variant(name: str, defines: list[str], verbose: bool = False) -> Path:
+    """A tuning build with extra -D flags: lib/variants/libpolykv_<name>.so,
+    loaded instead of the default library when PKV_LIB_VARIANT=<name>."""
+    out = LIB_DIR / "variants" / f"libpolykv_{name}.so"
+    return _compile(out, LIB_DIR / "variants" / f"obj_{name}", [f"-D{d}" for d in defines], verbose)
+
+
+def _compile(lib_path: Path, build_dir: Path, extra: list[str], verbose: bool) -> Path:
+    lib_path.parent.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     objs = []
-    build_dir = LIB_DIR / "obj"
-    build_dir.mkdir(exist_ok=True)
+    build_dir.mkdir(parents=True, exist_ok=True)
     procs = []
     for src in sources():
         obj = build_dir / (src.stem + ".o")
-        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cu":
             cmd.insert(1, "-Xptxas=-v" if verbose else "-Xptxas=-O3")
         if verbose:
@@ -74,13 +84,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for cmd, pr in procs:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    tmp = lib_path.with_suffix(".so.tmp")
     link = [nvcc, *ARCH_FLAGS, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB_PATH)
+    if "--variant" in sys.argv:  # --variant NAME DEF=VAL ...
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:], verbose="-v" in sys.argv))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB_PATH)

@@ -8,6 +8,7 @@ the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -71,7 +72,10 @@ class LibraryError(RuntimeError):
 
 
 def library_path() -> Path:
-    return LIB_PATH
+    """lib/libpolykv.so, or lib/variants/libpolykv_<name>.so when
+    PKV_LIB_VARIANT=<name> is set (tuning builds from _build.build_variant)."""
+    name = os.environ.get("PKV_LIB_VARIANT") or None
+    return LIB_PATH.parent / "variants" / f"libpolykv_{name}.so" if name else LIB_PATH
 
 
 def load() -> ctypes.CDLL:
@@ -82,12 +86,13 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if not LIB_PATH.exists():
+        path = library_path()
+        if not path.exists():
             raise LibraryError(
-                f"{LIB_PATH} not found: build it with `python -m paper_2604_24971_b200._build` "
+                f"{path} not found: build it with `python -m paper_2604_24971_b200._build` "
                 "or __graft_entry__.build(); there is no CPU fallback"
             )
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -22,6 +22,11 @@ struct Codebook3 {
 constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
 
 constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
+// relative guard of the paired fast path: q = RN(x * RN(1/s)) is within
+// 2^-23 |q| of x/s, so |q - n| + 2^-22 |q| <= 0.5 - 2^-20 (covering the
+// rounding of that sum) proves x/s rounds to n under any tie rule.
+constexpr float kKeyRel = 0x1p-22f;
+constexpr float kKeyAbs = 0x1p-20f;
 
 // Reference formula (keyquant.py:61-64), evaluated exactly as numpy does in
 // fp64: q = f64(x)/scale, code = floor(|q| + 0.5) * sign(q), clipped.
@@ -34,9 +39,28 @@ __device__ __forceinline__ int key_code_exact(float x, float s, int lo, int hi) 
   return (int)r;
 }
 
+// The same decision without fp64: |x|/s >= k + 0.5  <=>  fma(-(k + 0.5), s, |x|)
+// >= 0, and the FMA's single rounding keeps the sign of the exact difference.
+// The approximate quotient |x| * (1/s) is within 2^-22 relative of |x|/s, so
+// its nearest integer is off by at most one, next to a half-point; one test
+// each way fixes it. Needs s >= 1e-30 (1/s finite); ties round away from 0.
+__device__ __forceinline__ uint32_t key_code_fma(float x, float s, float rcp, int lo, int hi) {
+  const float ax = fabsf(x);
+  float r = rintf(ax * rcp);
+  if (fmaf(-(r - 0.5f), s, ax) < 0.f) {
+    r -= 1.f;
+  } else if (fmaf(-(r + 0.5f), s, ax) >= 0.f) {
+    r += 1.f;
+  }
+  int c = (int)r;
+  if (x < 0.f) c = -c;
+  return (uint32_t)max(lo, min(hi, c)) & 0xffu;
+}
+
 // 8 key codes of one chunk. Fast path: q = x * (1/s) rounded to nearest via
 // the 2^23 magic; the low byte of the magic sum is the two's-complement code.
-// Elements within kKeyEps of a half-point fall back to the exact formula.
+// Chunks with an element within kKeyEps of a half-point are re-coded exactly
+// (FMA half-point tests; fp64 only when force_exact, i.e. s < 1e-30).
 template <bool CLIP>
 __device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float rcp, bool force_exact) {
   float m[8];
@@ -58,7 +82,9 @@ __device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float r
     uint32_t c[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      c[j] = (s == 0.f) ? 0u : ((uint32_t)key_code_exact(x[j], s, CLIP ? -127 : -128, 127) & 0xffu);
+      c[j] = (s == 0.f) ? 0u
+             : force_exact ? ((uint32_t)key_code_exact(x[j], s, CLIP ? -127 : -128, 127) & 0xffu)
+                           : key_code_fma(x[j], s, rcp, CLIP ? -127 : -128, 127);
     w.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
     w.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
   }
@@ -80,11 +106,14 @@ __device__ __forceinline__ uint2 key_chunk_fast(const float (&x)[8], float2 rcp2
     const float2 m = __fadd2_rn(q, mg);
     const float2 n = __fadd2_rn(m, nmg);
     const float2 d = __ffma2_rn(n, make_float2(-1.f, -1.f), q);  // q - n, exact
-    worst = fmaxf(worst, fmaxf(fabsf(d.x), fabsf(d.y)));
+    // |q - x/s| <= 2^-23 |q|: the guard scales with |q| (|.| are free FFMA2 operand modifiers)
+    const float2 gq = __ffma2_rn(make_float2(fabsf(q.x), fabsf(q.y)), make_float2(kKeyRel, kKeyRel),
+                                 make_float2(fabsf(d.x), fabsf(d.y)));
+    worst = fmaxf(worst, fmaxf(gq.x, gq.y));
     mb[2 * j] = __float_as_uint(m.x);
     mb[2 * j + 1] = __float_as_uint(m.y);
   }
-  bad = worst > 0.5f - kKeyEps;
+  bad = worst > 0.5f - kKeyAbs;
   uint2 w;
   w.x = __byte_perm(__byte_perm(mb[0], mb[1], 0x0040), __byte_perm(mb[2], mb[3], 0x0040), 0x5410);
   w.y = __byte_perm(__byte_perm(mb[4], mb[5], 0x0040), __byte_perm(mb[6], mb[7], 0x0040), 0x5410);

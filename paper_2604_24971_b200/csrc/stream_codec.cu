@@ -19,10 +19,11 @@
 //
 // Per-tensor key scales (keyquant.py:55) need max|K| over a whole layer
 // before any key code can be written. The encode grid is split by role: value
-// CTAs stream V (ALU-bound), key CTAs run an absmax pass over every layer
-// (L2 evict_last), meet at a key-role barrier, then encode the keys walking
-// the layers in REVERSE order so the layers read last are still in L2. Each
-// SM runs a single code path (mixing both on one SM thrashes its I-cache).
+// CTAs stream V (ALU-bound), key CTAs run the absmax pass one layer ahead of
+// the key encode (L2 evict_last on the first read), so encoding layer l waits
+// only on per-layer completion counts that were met a segment earlier, and
+// re-reads layer l from L2. Each SM runs a single code path (mixing both on
+// one SM thrashes its I-cache).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -39,7 +40,10 @@ namespace stream {
 constexpr int kWarpsPerGroup = 4;
 constexpr int kGroupThreads = 32 * kWarpsPerGroup;
 constexpr int kEncGroups = 3;
-constexpr int kEncChunk = 16384;  // elements per encode work item
+#ifndef PKV_ENC_CHUNK
+#define PKV_ENC_CHUNK 16384
+#endif
+constexpr int kEncChunk = PKV_ENC_CHUNK;  // elements per encode work item
 constexpr int kDecChunk = 8192;   // elements per decode work item
 constexpr int kEncRingBytes = 192 * 1024;
 constexpr int kMaxL = kMaxLayers;
@@ -106,7 +110,7 @@ struct EncArgs {
   int num_layers, head_dim, k_mode, in_bytes;
   long long nvec, nelem;
   int nE, nV;  // items per layer
-  int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys
+  int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys, 4 no layer wait
   unsigned int total;
   float delta;
   Codebook3 cb;
@@ -114,9 +118,12 @@ struct EncArgs {
   uint32_t* status;
   uint32_t* replay_count;
   unsigned int* layer_max;  // [L] max |K| bits (published by the key-role CTAs)
-  unsigned int* key_barrier;  // arrivals of key-role CTAs after their absmax phase
+  unsigned int* layer_done;   // [L] absmax items folded into layer_max (per-tensor mode)
   int value_ctas;             // CTAs [0, value_ctas) encode values, the rest keys
   int nA;                     // absmax items per layer (per-tensor mode)
+  int nseg;                   // key-role segments of nE items: kind (A/E) + layer
+  uint8_t seg_absmax[2 * kMaxL];
+  uint8_t seg_layer[2 * kMaxL];
   const void* k_in[kMaxL];
   const void* v_in[kMaxL];
   int8_t* k_codes[kMaxL];
@@ -150,6 +157,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
 }
 __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -530,7 +546,7 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
   if (a.k_mode == PKV_K_TENSOR) {
-    const uint32_t pb = layer_max[it.layer];  // published at the key-role barrier, staged in smem
+    const uint32_t pb = layer_max[it.layer];  // staged in smem once layer_done[l] == nA
     const bool nonfinite = pb >= 0x7f800000u;
     const float s = (nonfinite || pb == 0) ? 0.f : __uint_as_float(pb) / 127.0f;  // f32(peak/127), keyquant.py:60
     if (it.idx == 0 && gt == 0) {
@@ -568,7 +584,13 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
       if (u * 8 >= n) continue;
       float x[8];
       lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
-      st_u2(dst + u * 8, key_chunk<false>(x, s, rcp, true));
+      uint32_t c[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        c[j] = exact_all ? (s == 0.f ? 0u : ((uint32_t)key_code_exact(x[j], s, -128, 127) & 0xffu))
+                         : key_code_fma(x[j], s, rcp, -128, 127);
+      st_u2(dst + u * 8, make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
+                                    c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
     }
     return;
   }
@@ -615,11 +637,13 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
 // ---------------------------------------------------------------------------
 // decode: key and value items
 // ---------------------------------------------------------------------------
-template <typename TOut>
+// B32: block32 keys (fp16 scales staged behind the codes); a separate
+// instantiation keeps that code (and its registers) out of the per-tensor kernel
+template <typename TOut, bool B32>
 __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, uint8_t* out, int gt) {
   const long long e0 = (long long)it.idx * kDecChunk;
   const int n = (int)min((long long)kDecChunk, a.nelem - e0);
-  const bool tensor = a.k_mode == PKV_K_TENSOR;
+  constexpr bool tensor = !B32;
   const float ts = tensor ? __ldg(a.k_scale[it.layer]) : 0.f;
   const __half* bsc = a.k_bscale[it.layer];
   const uint32_t out_s = tma::smem_u32(out);
@@ -786,9 +810,13 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
 // ---------------------------------------------------------------------------
 // Encode work lists. The grid is split by role (one code path per SM):
 //   value CTAs [0, value_ctas):  V(l, j) for all layers, layer-major;
-//   key CTAs:   A(l, j) for all layers (per-tensor mode), a key-role barrier,
-//               then E(l, j) with layers in REVERSE order, so the layers the
-//               absmax phase read last are still L2-resident.
+//   key CTAs (per-tensor mode): segments of nE items
+//     A(0) .. A(lag-1) | A(lag) E(0) | A(lag+1) E(1) | ... | E(L-1)
+//   i.e. the absmax pass runs `lag` layers ahead of the key encode, lag
+//   chosen so that the grid's in-flight stages fit in the gap: E(l) waits
+//   only for the A(l) items (counted in layer_done[l]), which every CTA has
+//   finished by then, and re-reads layer l while it is still in L2. Block32
+//   mode has no absmax: E(0) .. E(L-1).
 // Each CTA walks a static round-robin slice of its role's list.
 __device__ __forceinline__ Item enc_value_item_at(const EncArgs& a, long long t) {
   Item it{kValEnc, 0, 0, 0};
@@ -796,13 +824,9 @@ __device__ __forceinline__ Item enc_value_item_at(const EncArgs& a, long long t)
   it.idx = (int)(t - (long long)it.layer * a.nV);
   return it;
 }
-__device__ __forceinline__ Item enc_key_item_at(const EncArgs& a, long long t, bool absmax) {
-  Item it{absmax ? kAbsmax : kKeyEnc, 0, 0, 0};
-  const int per = absmax ? a.nA : a.nE;
-  const int r = (int)(t / per);
-  it.layer = absmax ? r : a.num_layers - 1 - r;
-  it.idx = (int)(t - (long long)r * per);
-  return it;
+__device__ __forceinline__ Item enc_key_item_at(const EncArgs& a, long long t) {
+  const int seg = (int)(t / a.nE);
+  return Item{a.seg_absmax[seg] ? kAbsmax : kKeyEnc, a.seg_layer[seg], (int)(t - (long long)seg * a.nE), 0};
 }
 
 __device__ __forceinline__ Item dec_item(const DecArgs& a, unsigned int t) {
@@ -842,7 +866,10 @@ struct EncPlan {
 template <int EB_OUT, int NG_>
 struct DecPlan {
   static constexpr int NG = NG_;
-  static constexpr int STAGE = kDecChunk + 1024;  // key codes + block32 scales / packed values + scales
+#ifndef PKV_DEC_STAGE_EXTRA
+#define PKV_DEC_STAGE_EXTRA 1024
+#endif
+  static constexpr int STAGE = kDecChunk + PKV_DEC_STAGE_EXTRA;  // key codes + block32 scales / packed values + scales
   static constexpr int OUT = kDecChunk * EB_OUT;
   static constexpr int NOB = 2;            // output buffers per group
   static constexpr int OUT_TOTAL = NG * NOB * OUT;
@@ -854,8 +881,10 @@ struct alignas(8) Ctl {
   uint64_t full[kMaxGroups][kMaxSG];
   uint64_t empty[kMaxGroups][kMaxSG];
   Item items[kMaxGroups][kMaxSG];
-  uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer, staged after the key barrier
-  uint32_t amax[kMaxL];       // encode: this CTA's absmax fold (shared atomics)
+  uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer, staged once layer_done is complete
+  uint32_t ready[kMaxL];      // encode: layer_max[l] staged
+  uint32_t gmax[kMaxGroups][kMaxSG];  // encode: absmax fold of the warps of one stage
+  uint32_t gcnt[kMaxGroups][kMaxSG];
 };
 
 template <int D, typename TIn>
@@ -957,7 +986,11 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       }
     tma::fence_mbar_init();
   }
-  if (threadIdx.x < kMaxL) ctl->amax[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxGroups * kMaxSG) {
+    (&ctl->gmax[0][0])[threadIdx.x] = 0;
+    (&ctl->gcnt[0][0])[threadIdx.x] = 0;
+  }
   __syncthreads();
   const bool value_role = (int)blockIdx.x < a.value_ctas;
 
@@ -996,47 +1029,15 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
       } else {
         const long long G = (long long)gridDim.x - a.value_ctas;
-        const long long b = (long long)blockIdx.x - a.value_ctas;
-        const long long ta = (long long)a.num_layers * a.nA, te = (long long)a.num_layers * a.nE;
-        long long t = b;
-        int phase = a.nA > 0 ? 0 : 2;  // 0 absmax, 1 barrier pending, 2 key encode
+        const long long total = (long long)a.nseg * a.nE;
+        long long t = (long long)blockIdx.x - a.value_ctas;
         auto next_item = [&]() -> Item {
-          if (phase == 0) {
-            if (t < ta) {
-              const Item it = enc_key_item_at(a, t, true);
-              t += G;
-              return it;
-            }
-            phase = 1;
-            t = b;
-            return Item{kBarrier, 0, 0, 0};
-          }
-          phase = 2;
-          if (t >= te) return Item{kEnd, 0, 0, 0};
-          const Item it = enc_key_item_at(a, t, false);
+          if (t >= total) return Item{kEnd, 0, 0, 0};
+          const Item it = enc_key_item_at(a, t);
           t += G;
           return it;
         };
-        auto barrier = [&]() {
-          // every absmax item of this CTA is folded into ctl->amax: publish,
-          // then wait for all key CTAs and stage the layer maxima
-          for (int l = 0; l < a.num_layers; ++l) {
-            const uint32_t m = ctl->amax[l];
-            if (m) atomicMax(a.layer_max + l, m);
-          }
-          __threadfence();
-          atomicAdd(a.key_barrier, 1u);
-          uint32_t spins = 0;
-          uint64_t t0 = 0;
-          while (*reinterpret_cast<volatile const uint32_t*>(a.key_barrier) < (uint32_t)G) {
-            __nanosleep(256);
-            tma::watchdog(spins, t0);
-          }
-          __threadfence();
-          for (int l = 0; l < a.num_layers; ++l)
-            ctl->layer_max[l] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + l);
-        };
-        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue, barrier);
+        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
       }
     }
     return;
@@ -1057,9 +1058,34 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     const bool skip = a.dbg == 1 || (a.dbg == 2 && it.kind == kValEnc) || (a.dbg == 3 && it.kind != kValEnc);
     if (it.kind == kAbsmax) {
       const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
-      if (lane == 0) atomicMax(&ctl->amax[it.layer], m);  // folded per CTA, published at the key barrier
+      if (lane == 0) {
+        // fold the group's warps; the last one publishes the item
+        atomicMax(&ctl->gmax[g][k], m);
+        __threadfence_block();
+        if (atomicAdd(&ctl->gcnt[g][k], 1u) == kWarpsPerGroup - 1) {
+          const uint32_t gm = atomicExch(&ctl->gmax[g][k], 0u);
+          ctl->gcnt[g][k] = 0;
+          if (gm) atomicMax(a.layer_max + it.layer, gm);
+          red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
+        }
+      }
     } else if (skip) {
     } else if (it.kind == kKeyEnc) {
+      if (a.nA && a.dbg != 4) {  // per-tensor scale: every absmax item of the layer must be in
+        if (lane == 0 && !*reinterpret_cast<volatile const uint32_t*>(&ctl->ready[it.layer])) {
+          uint32_t spins = 0;
+          uint64_t t0 = 0;
+          while (ld_acquire_u32(a.layer_done + it.layer) < (uint32_t)a.nA) {
+            __nanosleep(64);
+            tma::watchdog(spins, t0);
+          }
+          ctl->layer_max[it.layer] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + it.layer);
+          __threadfence_block();
+          *reinterpret_cast<volatile uint32_t*>(&ctl->ready[it.layer]) = 1u;
+        }
+        __threadfence_block();
+        __syncwarp();
+      }
       enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max);
     } else {
       enc_value_item<D, TIn, SYM, SIGN>(a, it, in_s, wig, lane, R, C);
@@ -1072,7 +1098,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
 // ---------------------------------------------------------------------------
 // decode kernel
 // ---------------------------------------------------------------------------
-template <int D, typename TOut, bool SIGN>
+template <int D, typename TOut, bool SIGN, bool B32>
 __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kernel(const __grid_constant__ DecArgs a) {
   using P = DecPlan<(int)sizeof(TOut), dec_groups<TOut>()>;
   using TL = Tile<D, (int)sizeof(TOut), kDecChunk>;
@@ -1113,7 +1139,7 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
           const uint32_t bytes = (uint32_t)min((long long)kDecChunk, a.nelem - e0);
           // block32: the item's fp16 scales follow the codes (whole 16-byte units;
           // a ragged last unit is read from global memory by the consumer)
-          const uint32_t sb = a.k_mode == PKV_K_TENSOR ? 0u : ((bytes + 31) / 32 * 2) & ~15u;
+          const uint32_t sb = B32 ? ((bytes + 31) / 32 * 2) & ~15u : 0u;
           tma::mbar_arrive_expect_tx(bar, bytes + sb);
           tma::bulk_g2s(in, a.k_codes[it.layer] + e0, bytes, bar, pol_first);
           if (sb) tma::bulk_g2s(in + kDecChunk, a.k_bscale[it.layer] + (e0 >> 5), sb, bar, pol_first);
@@ -1145,7 +1171,7 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
     int nv = 0;
     long long v0 = 0;
     if (it.kind == kKeyDec) {
-      dec_key_item<TOut>(a, it, tma::smem_u32(in), out, gt);
+      dec_key_item<TOut, B32>(a, it, tma::smem_u32(in), out, gt);
     } else {
       v0 = (long long)it.idx * TL::VR;
       nv = (int)min((long long)TL::VR, a.nvec - v0);
@@ -1261,8 +1287,12 @@ int enc_launch(const EncArgs& a, int d, bool sym, bool sign, cudaStream_t st) {
 template <int D, typename TOut>
 int dec_launch_d(const DecArgs& a, bool sign, cudaStream_t st) {
   const size_t smem = dec_smem_bytes<TOut>();
-  return sign ? coop_launch(dec_kernel<D, TOut, true>, &a, smem, threads_for<dec_groups<TOut>()>(), st)
-              : coop_launch(dec_kernel<D, TOut, false>, &a, smem, threads_for<dec_groups<TOut>()>(), st);
+  constexpr int T = threads_for<dec_groups<TOut>()>();
+  if (a.k_mode == PKV_K_TENSOR)
+    return sign ? coop_launch(dec_kernel<D, TOut, true, false>, &a, smem, T, st)
+                : coop_launch(dec_kernel<D, TOut, false, false>, &a, smem, T, st);
+  return sign ? coop_launch(dec_kernel<D, TOut, true, true>, &a, smem, T, st)
+              : coop_launch(dec_kernel<D, TOut, false, true>, &a, smem, T, st);
 }
 
 template <typename TOut>
@@ -1356,13 +1386,37 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   const int dk = do_v ? r.head_dim : 64;  // key-only launches never touch the value tile geometry
   if (rc == PKV_OK) {
     a->nA = (do_k && r.k_mode == PKV_K_TENSOR) ? a->nE : 0;
-    a->key_barrier = w32 + L;
+    a->layer_done = w32 + L;
     const int grid = sm_count();  // one CTA per SM (checked by the launcher)
+    // key-role segment order (see enc_key_item_at)
+    a->nseg = 0;
+    if (a->nA) {
+      // lag: enough layers that the key CTAs' in-flight stages (~3 rings per
+      // CTA) cannot reach E(l) before every A(l) item has been consumed
+      int lag = 4;
+      if (const char* f = std::getenv("PKV_KEY_LAG")) lag = std::max(1, std::atoi(f));
+      for (int j = 0; j < L + lag; ++j) {
+        if (j < L) {
+          a->seg_absmax[a->nseg] = 1;
+          a->seg_layer[a->nseg++] = (uint8_t)j;
+        }
+        if (j >= lag && j - lag < L) {
+          a->seg_absmax[a->nseg] = 0;
+          a->seg_layer[a->nseg++] = (uint8_t)(j - lag);
+        }
+      }
+    } else if (do_k) {
+      for (int l = 0; l < L; ++l) {
+        a->seg_absmax[a->nseg] = 0;
+        a->seg_layer[a->nseg++] = (uint8_t)l;
+      }
+    }
     int key_ctas = 0;
     if (do_k && do_v) {
-      // share of SMs for the key role (swept on C3 bf16: 0.3 -> 328 us, 0.4 -> 296 us,
-      // 0.5 -> 341 us); PKV_KEY_SM_FRACTION overrides
-      double frac = 0.4;
+      // share of SMs for the key role (swept on C3 bf16 with the lagged
+      // absmax: 0.3 -> 316 us, 0.35 -> 270 us, 0.4 -> 285 us);
+      // PKV_KEY_SM_FRACTION overrides
+      double frac = 0.35;
       if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
       key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
     } else if (do_k) {

@@ -11,6 +11,7 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--kmode", default="tensor")
+ap.add_argument("--eager", action="store_true", help="no CUDA graph (includes host launch overhead)")
 ap.add_argument("--path", default="stream", choices=["stream", "warp"])
 a = ap.parse_args()
 import os
@@ -25,7 +26,21 @@ ks = [k for k, _ in dump.layers]; vs = [v for _, v in dump.layers]
 arena = _Arena(g, L, a.kmode, dev)
 none = [None] * L
 
+def graph(fn):
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        fn()
+    torch.cuda.current_stream().wait_stream(st)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        fn()
+    return gr.replay
+
+
 def timeit(fn):
+    if not a.eager:
+        fn = graph(fn)
     for _ in range(3): fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -48,4 +63,4 @@ inb = 2 if a.dtype == "bf16" else 4
 bytes_ = {"enc_k": n * (inb + 1), "enc_v": n * (inb + 3 / 8) + 4 * n / D, "dec_k": 3 * n, "dec_v": n * (2 + 3 / 8) + 4 * n / D}
 bytes_["enc_kv"] = bytes_["enc_k"] + bytes_["enc_v"]; bytes_["dec_kv"] = bytes_["dec_k"] + bytes_["dec_v"]
 print(a.config, a.dtype, a.path, json.dumps({k: {"ms": round(v, 4), "GBs": round(bytes_[k] / v / 1e6, 1)} for k, v in res.items()}))
-print("replays", int(arena.replay.item()))
+print("replays", int(arena.replay.item()), flush=True)
