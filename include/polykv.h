@@ -163,10 +163,11 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim,
                          void* stream);
 
 /* Internal self-checks that need the device. PKV_SELFTEST_DIVISION runs the
- * decode kernel's correctly-rounded x / f32(sqrt(d)) sequence against IEEE
- * division over every f32 mantissa for d in {8, 32, 128}; returns the number
- * of mismatches (0 expected) or a negative PKV_ERR_* code. Synchronises
- * `stream`. scratch: >= 12 bytes of device memory. */
+ * decode kernel's correctly-rounded x / f32(sqrt(d)) sequence for d in
+ * {8, 32, 128} and the block32 key-scale x / 127 sequence against IEEE
+ * division over every f32 mantissa; returns the number of mismatches
+ * (0 expected) or a negative PKV_ERR_* code. Synchronises `stream`.
+ * scratch: >= 16 bytes of device memory. */
 #define PKV_SELFTEST_DIVISION 1
 int64_t pkv_selftest(int what, void* scratch, size_t scratch_bytes, void* stream);
 

@@ -803,6 +803,18 @@ __global__ void selftest_div_kernel(uint32_t* mismatches) {
   if (bad) atomicAdd(mismatches, bad);
 }
 
+// The same for div127 (block32 key scales).
+__global__ void selftest_div127_kernel(uint32_t* mismatches) {
+  uint32_t bad = 0;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < (1u << 23); m += gridDim.x * blockDim.x) {
+    const float x = __uint_as_float(0x3f800000u | m);
+    bad += __float_as_uint(div127(x)) != __float_as_uint(__fdiv_rn(x, 127.0f));
+    bad += __float_as_uint(div127(x * 0x1p-90f)) != __float_as_uint(__fdiv_rn(x * 0x1p-90f, 127.0f));
+    bad += __float_as_uint(div127(x * 0x1p+90f)) != __float_as_uint(__fdiv_rn(x * 0x1p+90f, 127.0f));
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}
+
 }  // namespace pkv
 
 // ===========================================================================
@@ -1171,17 +1183,18 @@ int pkv_pack_codes(const uint8_t* codes, int64_t count, uint8_t* packed, uint32_
 
 int64_t pkv_selftest(int what, void* scratch, size_t scratch_bytes, void* stream) {
   if (what != PKV_SELFTEST_DIVISION) return PKV_ERR_INVALID_ARG;
-  if (!scratch || scratch_bytes < 3 * sizeof(uint32_t)) return PKV_ERR_WORKSPACE;
+  if (!scratch || scratch_bytes < 4 * sizeof(uint32_t)) return PKV_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint32_t* cnt = static_cast<uint32_t*>(scratch);
-  if (cudaMemsetAsync(cnt, 0, 3 * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
+  if (cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
   selftest_div_kernel<8><<<1024, 256, 0, st>>>(cnt + 0);
   selftest_div_kernel<32><<<1024, 256, 0, st>>>(cnt + 1);
   selftest_div_kernel<128><<<1024, 256, 0, st>>>(cnt + 2);
-  uint32_t host[3] = {0, 0, 0};
+  selftest_div127_kernel<<<1024, 256, 0, st>>>(cnt + 3);
+  uint32_t host[4] = {0, 0, 0, 0};
   if (cudaMemcpyAsync(host, cnt, sizeof(host), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PKV_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return PKV_ERR_CUDA;
-  return (int64_t)host[0] + host[1] + host[2];
+  return (int64_t)host[0] + host[1] + host[2] + host[3];
 }
 
 }  // extern "C"

@@ -22,9 +22,10 @@ struct Codebook3 {
 constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
 
 constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
-// relative guard of the paired fast path: q = RN(x * RN(1/s)) is within
-// 2^-23 |q| of x/s, so |q - n| + 2^-22 |q| <= 0.5 - 2^-20 (covering the
-// rounding of that sum) proves x/s rounds to n under any tie rule.
+// relative guard of the paired fast path: q = RN(x * r) with r within 1 ulp
+// of 1/s (RN(1/s) or rcp.approx) is within 1.5 * 2^-23 |q| of x/s, so
+// |q - n| + 2^-22 |q| <= 0.5 - 2^-20 (covering the rounding of that sum)
+// proves x/s rounds to n under any tie rule.
 constexpr float kKeyRel = 0x1p-22f;
 constexpr float kKeyAbs = 0x1p-20f;
 
@@ -123,6 +124,29 @@ __device__ __forceinline__ uint2 key_chunk_fast(const float (&x)[8], float2 rcp2
 // int8 code -> exact f32 via the 2^23 magic (no I2F on the conversion pipe)
 __device__ __forceinline__ float i8_to_f32(uint32_t word_x80, int byte) {
   return __uint_as_float(__byte_perm(word_x80, 0x4B000000u, 0x7650 + byte)) - 8388736.0f;
+}
+
+// x / c correctly rounded for the constant c = 127 (block32 key scales,
+// keyquant.py:60 applied per block): q = x*r corrected once with the exact FMA
+// remainder, verified over every f32 mantissa by pkv_selftest; inputs outside
+// [2^-100, 2^100] take IEEE division.
+constexpr float kRcp127 = 1.0f / 127.0f;
+__device__ __forceinline__ float div127_core(float x) {  // |x| in [2^-100, 2^100]
+  const float q = x * kRcp127;
+  const float e = fmaf(-q, 127.0f, x);
+  return fmaf(e, kRcp127, q);
+}
+__device__ __forceinline__ float div127(float x) {
+  const float ax = fabsf(x);
+  if (!(ax >= 0x1p-100f && ax <= 0x1p100f)) return __fdiv_rn(x, 127.0f);
+  return div127_core(x);
+}
+
+// 1/x within 1 ulp (PTX rcp.approx.f32), for normal x
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // x / f32(sqrt(D)), correctly rounded. Power-of-four D: exact multiply.

@@ -44,6 +44,20 @@ constexpr int kEncGroups = 3;
 #define PKV_ENC_CHUNK 16384
 #endif
 constexpr int kEncChunk = PKV_ENC_CHUNK;  // elements per encode work item
+#ifndef PKV_B32_UNROLL
+#define PKV_B32_UNROLL 2
+#endif
+constexpr int kB32Unroll = PKV_B32_UNROLL;  // block32 key encode: chunks in flight per lane
+#ifndef PKV_KEY_EARLY_RELEASE
+#define PKV_KEY_EARLY_RELEASE 1
+#endif
+constexpr bool kKeyEarlyRelease = PKV_KEY_EARLY_RELEASE;
+#ifndef PKV_ROLE_MAP
+#define PKV_ROLE_MAP 0  // 0: roles by block index, 1: by SM id (measured slightly slower)
+#endif
+#ifndef PKV_SIGNPACK
+#define PKV_SIGNPACK 1  // value codes packed from sign bits by funnel shifts
+#endif  // bf16 key items: copy to registers, release the stage
 constexpr int kDecChunk = 8192;   // elements per decode work item
 constexpr int kEncRingBytes = 192 * 1024;
 constexpr int kMaxL = kMaxLayers;
@@ -433,6 +447,37 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
       float gacc[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) gacc[k] = INFINITY;
+#if PKV_SIGNPACK
+      // Codes from sign bits. s_k = sign(|u| - t_k N) is a thermometer code
+      // (t1 < t2 < t3), mm = s1 + s2 + s3 = #thresholds above |u| has
+      // bit1 = s2 and bit0 = s1^s2^s3, and code = negative ? mm : 7 - mm.
+      // So, with n = sign(u): code bits (2,1,0) = ~(n, s2^n, s1^s2^s3^n):
+      // the complemented bits are shifted into the word MSB-first (one
+      // funnel shift each, coordinate 7 of the chunk first) and the word is
+      // complemented once at the end.
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const int p = (q & ~7) | (7 - (q & 7));  // e = 7 .. 0 within each chunk pair
+        const float2 u = xp[p];
+        const float2 au = f2(fabsf(u.x), fabsf(u.y));
+        const float2 d1 = __fadd2_rn(au, T1), d2 = __fadd2_rn(au, T2), d3 = __fadd2_rn(au, T3);
+        float& ga = gacc[(2 * p) & 3];
+        float& gb = gacc[(2 * p + 1) & 3];
+        ga = fminf(ga, fminf(fabsf(d1.x), fabsf(d1.y)));
+        gb = fminf(gb, fminf(fabsf(d2.x), fabsf(d2.y)));
+        ga = fminf(ga, fminf(fabsf(d3.x), fabsf(d3.y)));
+        gb = fminf(gb, fminf(au.x, au.y));
+        const int c0 = (p >> 3) * 2;
+        const uint32_t ux = __float_as_uint(u.x), uy = __float_as_uint(u.y);
+        const uint32_t b1x = __float_as_uint(d2.x) ^ ux, b1y = __float_as_uint(d2.y) ^ uy;
+        const uint32_t b0x = __float_as_uint(d1.x) ^ __float_as_uint(d3.x) ^ b1x;
+        const uint32_t b0y = __float_as_uint(d1.y) ^ __float_as_uint(d3.y) ^ b1y;
+        words[c0] = __funnelshift_l(b0x, __funnelshift_l(b1x, __funnelshift_l(ux, words[c0], 1), 1), 1);
+        words[c0 + 1] = __funnelshift_l(b0y, __funnelshift_l(b1y, __funnelshift_l(uy, words[c0 + 1], 1), 1), 1);
+      }
+#pragma unroll
+      for (int c = 0; c < NCL; ++c) words[c] = ~words[c] & 0xffffffu;
+#else
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         const float2 u = xp[p];
@@ -453,6 +498,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         words[c0] += cx << (3 * e);  // disjoint fields: + == |, one LEA
         words[c0 + 1] += cy << (3 * e);
       }
+#endif
       const float g = fminf(fminf(gacc[0], gacc[1]), fminf(gacc[2], gacc[3]));
       replay |= g < DL;
     } else {
@@ -539,9 +585,12 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
   return m;
 }
 
-template <typename TIn>
+// release() hands the input stage back to the producer; a path that has
+// copied the stage into registers calls it before computing (and the caller
+// then must not release again: `released` is set).
+template <typename TIn, class Release>
 __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane,
-                             const uint32_t* layer_max) {
+                             const uint32_t* layer_max, Release release, bool& released) {
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
@@ -555,9 +604,49 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     }
     const float rcp = 1.0f / s;
     const bool exact_all = !(s >= 1e-30f);
+    constexpr int ITERS = kEncChunk / 8 / kGroupThreads;
+    if constexpr (sizeof(TIn) == 2 && kKeyEarlyRelease) {
+      if (n == kEncChunk && !exact_all) {
+        // bf16 full item: the lane's 16 chunks (64 registers) are copied out
+        // and the stage released at once, so its refill overlaps the math.
+        // Branch-free pass; chunks near a half-point are re-coded from global
+        // memory afterwards (rare; the stage may be refilled by then)
+        uint4 raw[ITERS];
+#pragma unroll
+        for (int i = 0; i < ITERS; ++i) raw[i] = tma::lds128(in_s + (i * kGroupThreads + gt) * 16);
+        release();
+        released = true;
+        uint32_t need = 0;
+#pragma unroll
+        for (int i = 0; i < ITERS; ++i) {
+          const int u = i * kGroupThreads + gt;
+          float x[8];
+          x[0] = bf16lo(raw[i].x); x[1] = bf16hi(raw[i].x); x[2] = bf16lo(raw[i].y); x[3] = bf16hi(raw[i].y);
+          x[4] = bf16lo(raw[i].z); x[5] = bf16hi(raw[i].z); x[6] = bf16lo(raw[i].w); x[7] = bf16hi(raw[i].w);
+          bool bad;
+          st_u2(dst + u * 8, key_chunk_fast(x, make_float2(rcp, rcp), bad));
+          need |= (uint32_t)bad << i;
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const TIn*>(a.k_in[it.layer]) + e0);
+#pragma unroll 1
+        while (need) {
+          const int i = __ffs(need) - 1;
+          need &= need - 1;
+          const int u = i * kGroupThreads + gt;
+          const uint4 r = __ldg(src + u);
+          const float x[8] = {bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y),
+                              bf16lo(r.z), bf16hi(r.z), bf16lo(r.w), bf16hi(r.w)};
+          uint32_t c[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) c[j] = key_code_fma(x[j], s, rcp, -128, 127);
+          st_u2(dst + u * 8, make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
+                                        c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
+        }
+        return;
+      }
+    }
     // branch-free fast pass over the whole item; chunks near a rounding
     // half-point are re-coded exactly afterwards (rare)
-    constexpr int ITERS = kEncChunk / 8 / kGroupThreads;
     uint32_t need = 0;
     auto chunk = [&](int i) {
       const int u = i * kGroupThreads + gt;
@@ -596,41 +685,59 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
   }
   // block32: one fp16 scale per 32 contiguous elements; 4 consecutive lanes own a block
   __half* bsc = a.k_bscale[it.layer];
-#pragma unroll 2
+#pragma unroll kB32Unroll
   for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
     const int u = i * kGroupThreads + gt;
     const bool valid = u * 8 < n;
-    float x[8];
-    uint32_t m = 0;
-    if (valid) {
-      lds_chunk8<TIn>(in_s + u * 8 * (int)sizeof(TIn), in_s + u * 8 * (int)sizeof(TIn) + 16, x);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m = max(m, __float_as_uint(x[j]) & 0x7fffffffu);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = 0.f;
-    }
+    const uint32_t a0 = in_s + u * 8 * (int)sizeof(TIn);
+    uint32_t m = valid ? lds_absmax8<TIn>(a0) : 0u;  // max |x| bits of the lane's 8
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
     if (!valid) continue;
-    const bool nonfinite = m >= 0x7f800000u;
-    uint16_t s16b = __half_as_ushort(__float2half_rn(__uint_as_float(m) / 127.0f));
-    bool overflow = false;
-    if (nonfinite || m == 0) {
-      s16b = 0;
-    } else if ((s16b & 0x7fffu) >= 0x7c00u) {
-      overflow = true;
-      s16b = 0;
-    } else if (s16b == 0) {
-      s16b = 1;  // peak > 0 but the scale underflows fp16: smallest subnormal
+    float x[8];
+    lds_chunk8<TIn>(a0, a0 + 16, x);
+    // f16(f32(peak / 127)) (keyquant.py:60 per block, then the fp16 store)
+    const float pk = __uint_as_float(m);
+    const bool in_range = m >= 0x0d800000u && m <= 0x71800000u;  // [2^-100, 2^100]: div127's verified range
+    uint16_t s16b = __half_as_ushort(__float2half_rn(div127_core(pk)));
+    const uint32_t ex = s16b & 0x7c00u;
+    uint2 w;
+    if (in_range && ex != 0u && ex != 0x7c00u) {
+      // normal fp16 scale: s >= (peak/127)(1 - 2^-11), so |x|/s < 127.07 and
+      // the clip never acts; paired fast path (rcp.approx is within 1 ulp,
+      // inside the kKeyRel guard), FMA-exact re-code near a half-point
+      const float s = __half2float(__ushort_as_half(s16b));
+      const float rcp = rcp_approx(s);
+      bool bad;
+      w = key_chunk_fast(x, make_float2(rcp, rcp), bad);
+      if (bad) {
+        uint32_t c[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = key_code_fma(x[j], s, rcp, -127, 127);
+        w = make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24), c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24));
+      }
+    } else {
+      // zero / non-finite peak, fp16 overflow or underflow, extreme range
+      const bool nonfinite = m >= 0x7f800000u;
+      s16b = __half_as_ushort(__float2half_rn(__fdiv_rn(pk, 127.0f)));
+      bool overflow = false;
+      if (nonfinite || m == 0) {
+        s16b = 0;
+      } else if ((s16b & 0x7fffu) >= 0x7c00u) {
+        overflow = true;
+        s16b = 0;
+      } else if (s16b == 0) {
+        s16b = 1;  // peak > 0 but the scale underflows fp16: smallest subnormal
+      }
+      if ((lane & 3) == 0) {
+        if (nonfinite) atomicOr(&a.status[it.layer], PKV_FLAG_K_NONFINITE);
+        if (overflow) atomicOr(&a.status[it.layer], PKV_FLAG_K_SCALE_OVERFLOW);
+      }
+      const float s = __half2float(__ushort_as_half(s16b));
+      w = key_chunk<true>(x, s, 1.0f / s, !(s >= 1e-30f));
     }
-    const float s = __half2float(__ushort_as_half(s16b));
-    if ((lane & 3) == 0) {
-      bsc[(e0 + u * 8) >> 5] = __ushort_as_half(s16b);
-      if (nonfinite) atomicOr(&a.status[it.layer], PKV_FLAG_K_NONFINITE);
-      if (overflow) atomicOr(&a.status[it.layer], PKV_FLAG_K_SCALE_OVERFLOW);
-    }
-    st_u2(dst + u * 8, key_chunk<true>(x, s, 1.0f / s, !(s >= 1e-30f)));
+    if ((lane & 3) == 0) bsc[(e0 + u * 8) >> 5] = __ushort_as_half(s16b);
+    st_u2(dst + u * 8, w);
   }
 }
 
@@ -992,7 +1099,18 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     (&ctl->gcnt[0][0])[threadIdx.x] = 0;
   }
   __syncthreads();
-  const bool value_role = (int)blockIdx.x < a.value_ctas;
+  // Role split. SMs that share instruction caches (same TPC / GPC) should run
+  // the same code path, so the key role takes a contiguous range of SM ids
+  // (the grid is one CTA per SM: %smid is a permutation of 0..grid-1).
+  // Ranks are dense within each role.
+  const unsigned gk = gridDim.x - (unsigned)a.value_ctas;
+  unsigned pos = blockIdx.x;
+#if PKV_ROLE_MAP == 1
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(pos));
+  if (pos >= gridDim.x) pos = blockIdx.x;  // not a dense numbering: fall back to block order
+#endif
+  const bool value_role = pos < (unsigned)a.value_ctas;
+  const long long role_rank = value_role ? (long long)pos : (long long)pos - a.value_ctas;
 
   if (warp == 0) {
     // ---------------- producer ----------------
@@ -1019,7 +1137,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       };
       if (value_role) {
         const long long G = a.value_ctas, total = (long long)a.num_layers * a.nV;
-        long long t = blockIdx.x;
+        long long t = role_rank;
         auto next_item = [&]() -> Item {
           if (t >= total) return Item{kEnd, 0, 0, 0};
           const Item it = enc_value_item_at(a, t);
@@ -1030,7 +1148,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       } else {
         const long long G = (long long)gridDim.x - a.value_ctas;
         const long long total = (long long)a.nseg * a.nE;
-        long long t = (long long)blockIdx.x - a.value_ctas;
+        long long t = role_rank;
         auto next_item = [&]() -> Item {
           if (t >= total) return Item{kEnd, 0, 0, 0};
           const Item it = enc_key_item_at(a, t);
@@ -1056,6 +1174,11 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     if (it.kind == kEnd) break;
     const uint32_t in_s = tma::smem_u32(ring + (g * NSG + k) * P::STAGE);
     const bool skip = a.dbg == 1 || (a.dbg == 2 && it.kind == kValEnc) || (a.dbg == 3 && it.kind != kValEnc);
+    bool released = false;
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);
+    };
     if (it.kind == kAbsmax) {
       const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
       if (lane == 0) {
@@ -1086,12 +1209,11 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         __threadfence_block();
         __syncwarp();
       }
-      enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max);
+      enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max, release, released);
     } else {
       enc_value_item<D, TIn, SYM, SIGN>(a, it, in_s, wig, lane, R, C);
     }
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);  // this warp is done with the stage
+    if (!released) release();  // this warp is done with the stage
   }
 }
 
@@ -1413,10 +1535,12 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
     }
     int key_ctas = 0;
     if (do_k && do_v) {
-      // share of SMs for the key role (swept on C3 bf16 with the lagged
-      // absmax: 0.3 -> 316 us, 0.35 -> 270 us, 0.4 -> 285 us);
-      // PKV_KEY_SM_FRACTION overrides
-      double frac = 0.35;
+      // share of SMs for the key role, swept on C3 bf16 (tools/ab_frac.sh):
+      // per-tensor 0.32 -> 343 us, 0.35 -> 287, 0.378 -> 269, 0.405 -> 278;
+      // block32 (one key pass) 0.36 -> 336, 0.4 -> 302, 0.43 -> 285. The curve is not
+      // smooth: SMs sharing instruction caches should run one role, so
+      // where the role boundary falls matters. PKV_KEY_SM_FRACTION overrides
+      double frac = r.k_mode == PKV_K_TENSOR ? 0.38 : 0.43;
       if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
       key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
     } else if (do_k) {

@@ -240,10 +240,10 @@ def test_decode_attention_matches_fp64_oracle():
 
 
 def test_decode_division_sequence_is_correctly_rounded():
-    # exhaustive over all f32 mantissas for d in {8, 32, 128} (pkv_selftest)
+    # exhaustive over all f32 mantissas: x / f32(sqrt(d)) for d in {8, 32, 128} and x / 127 (pkv_selftest)
     from paper_2604_24971_b200 import _lib
 
-    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")  # 4 counters
     n = _lib.load().pkv_selftest(1, scratch.data_ptr(), 16, torch.cuda.current_stream().cuda_stream)
     assert n == 0, f"{n} mismatches vs IEEE division"
 

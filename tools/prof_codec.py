@@ -14,6 +14,7 @@ ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--attn", action="store_true")
 ap.add_argument("--only", default="kv")
+ap.add_argument("--kmode", default="tensor")
 a = ap.parse_args()
 L, H, D, T = {"c3": (32, 8, 128, 4096), "c2": (24, 32, 64, 1851)}[a.config]
 dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
@@ -21,9 +22,9 @@ g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
 dev = torch.device("cuda")
 dump = pk.synth_gaussian_dump(g, seed=0, device=dev, dtype=dt, generator="torch")
 ks = [k for k, _ in dump.layers]; vs = [v for _, v in dump.layers]
-arena = _Arena(g, L, "tensor", dev)
+arena = _Arena(g, L, a.kmode, dev)
 for _ in range(a.iters):
-    kb, vb, _ = _encode_layers(ks if "k" in a.only else [None]*L, vs if "v" in a.only else [None]*L, g, pk.GAUSSIAN_3BIT, None, "tensor", device=dev, arena=arena, check=False)
+    kb, vb, _ = _encode_layers(ks if "k" in a.only else [None]*L, vs if "v" in a.only else [None]*L, g, pk.GAUSSIAN_3BIT, None, a.kmode, device=dev, arena=arena, check=False)
 if a.only == "kv":
     pool = pk.SharedPool(g, list(zip(kb, vb))).seal()
     for _ in range(a.iters):
