@@ -52,6 +52,10 @@ constexpr int kB32Unroll = PKV_B32_UNROLL;  // block32 key encode: chunks in fli
 #define PKV_KEY_EARLY_RELEASE 1
 #endif
 constexpr bool kKeyEarlyRelease = PKV_KEY_EARLY_RELEASE;
+#ifndef PKV_KEY_DYNAMIC
+#define PKV_KEY_DYNAMIC 1  // per-tensor keys: readiness-driven A/E order (else static segments)
+#endif
+constexpr bool kKeyDynamic = PKV_KEY_DYNAMIC;
 #ifndef PKV_ROLE_MAP
 #define PKV_ROLE_MAP 0  // 0: roles by block index, 1: by SM id (measured slightly slower)
 #endif
@@ -136,6 +140,7 @@ struct EncArgs {
   int value_ctas;             // CTAs [0, value_ctas) encode values, the rest keys
   int nA;                     // absmax items per layer (per-tensor mode)
   int nseg;                   // key-role segments of nE items: kind (A/E) + layer
+  int key_lag;                // absmax layers allowed ahead of the key encode
   uint8_t seg_absmax[2 * kMaxL];
   uint8_t seg_layer[2 * kMaxL];
   const void* k_in[kMaxL];
@@ -1145,7 +1150,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
           return it;
         };
         produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
-      } else {
+      } else if (a.nA == 0 || !kKeyDynamic) {
         const long long G = (long long)gridDim.x - a.value_ctas;
         const long long total = (long long)a.nseg * a.nE;
         long long t = role_rank;
@@ -1154,6 +1159,54 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
           const Item it = enc_key_item_at(a, t);
           t += G;
           return it;
+        };
+        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
+      } else {
+        // Per-tensor keys, readiness-driven order: two cursors over this
+        // CTA's slice of the absmax list A and the key-encode list E (both
+        // layer-major, nA == nE items per layer). An E item of layer l is
+        // issued only once every CTA's A(l) items are folded (layer_done[l]),
+        // after the producer has staged layer_max[l] in shared memory, so no
+        // consumer ever holds a stage waiting for a scale; while layer l is
+        // not ready the producer issues absmax items instead, at most `lag`
+        // layers ahead of the encode cursor (L2 footprint).
+        const long long G = (long long)gridDim.x - a.value_ctas;
+        const long long totA = (long long)a.num_layers * a.nA, totE = (long long)a.num_layers * a.nE;
+        long long ta = role_rank, te = role_rank;
+        int ready = -1;  // layers [0, ready] staged in ctl->layer_max
+        auto stage = [&](int l) {
+          ctl->layer_max[l] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + l);
+          __threadfence_block();
+          *reinterpret_cast<volatile uint32_t*>(&ctl->ready[l]) = 1u;
+          ready = l;
+        };
+        auto next_item = [&]() -> Item {
+          for (;;) {
+            if (te >= totE) return Item{kEnd, 0, 0, 0};
+            const int el = (int)(te / a.nE);
+            if (el <= ready) {
+              const Item it{kKeyEnc, el, (int)(te - (long long)el * a.nE), 0};
+              te += G;
+              return it;
+            }
+            if (ld_acquire_u32(a.layer_done + el) >= (uint32_t)a.nA) {
+              stage(el);
+              continue;
+            }
+            if (ta < totA && ta / a.nA < (long long)el + a.key_lag) {
+              const int al = (int)(ta / a.nA);
+              const Item it{kAbsmax, al, (int)(ta - (long long)al * a.nA), 0};
+              ta += G;
+              return it;
+            }
+            uint32_t spins = 0;
+            uint64_t t0 = 0;
+            while (ld_acquire_u32(a.layer_done + el) < (uint32_t)a.nA) {
+              __nanosleep(128);
+              tma::watchdog(spins, t0);
+            }
+            stage(el);
+          }
         };
         produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
       }
@@ -1517,6 +1570,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // CTA) cannot reach E(l) before every A(l) item has been consumed
       int lag = 4;
       if (const char* f = std::getenv("PKV_KEY_LAG")) lag = std::max(1, std::atoi(f));
+      a->key_lag = lag;
       for (int j = 0; j < L + lag; ++j) {
         if (j < L) {
           a->seg_absmax[a->nseg] = 1;

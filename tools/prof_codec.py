@@ -15,6 +15,7 @@ ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--attn", action="store_true")
 ap.add_argument("--only", default="kv")
 ap.add_argument("--kmode", default="tensor")
+ap.add_argument("--dec", default="kv", help="decode keys (k), values (v) or both")
 a = ap.parse_args()
 L, H, D, T = {"c3": (32, 8, 128, 4096), "c2": (24, 32, 64, 1851)}[a.config]
 dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
@@ -28,7 +29,7 @@ for _ in range(a.iters):
 if a.only == "kv":
     pool = pk.SharedPool(g, list(zip(kb, vb))).seal()
     for _ in range(a.iters):
-        pool.decode_layers(None, torch.bfloat16)
+        pool.decode_layers(None, torch.bfloat16, keys="k" in a.dec, values="v" in a.dec)
 if a.attn:
     q = torch.randn(15, H, 4, D, device=dev, dtype=torch.bfloat16)
     for _ in range(a.iters):

@@ -4,7 +4,11 @@ import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
-hdr, data = rows[1], rows[2:]
+hdr, data = rows[1], []
+for r in rows[2:]:  # first kernel only (a capture of several repeats the header)
+    if r and r[0] in ("Kernel Name", "Address"):
+        break
+    data.append(r)
 col = {h: i for i, h in enumerate(hdr)}
 reasons = ["stall_long_sb", "stall_wait", "stall_short_sb", "stall_branch_resolving", "stall_membar", "stall_lg",
            "stall_mio", "stall_math", "stall_sleep", "stall_selected", "stall_not_selected", "stall_no_inst"]
