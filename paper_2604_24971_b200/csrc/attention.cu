@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
 
   // ---- Q row tile, pre-scaled by softmax_scale * log2(e): Qs[d][r] ----
   // (8 consecutive d per thread: one 16-byte load for bf16 queries)
+  // (consecutive threads take consecutive rows: the transposed stores
+  // Qs[d][r] are bank-conflict free)
   for (int i = tid; i < RT * D / 8; i += kAttnThreads2) {
-    const int r = i / (D / 8), d0 = (i % (D / 8)) * 8;
+    const int r = i % RT, d0 = (i / RT) * 8;
     const int row = r0 + r;
     float qv[8];
     if (row < a.rows) {
@@ -181,7 +183,13 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
   // stage the packed tile [t0, t0 + nt) of head h into raw shared memory
   auto stage = [&](long long t0, int nt) {
     const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
-    for (int i = tid; i < nt * D / 16; i += kAttnThreads2) cp_async16(rk + i * 16, gk + i * 16);
+    // 16-byte chunk c of token t lands in slot c ^ (t % (D/16)) of its row, so
+    // the dequant's column reads (consecutive tokens, one chunk) are
+    // bank-conflict free
+    for (int i = tid; i < nt * D / 16; i += kAttnThreads2) {
+      const int t = i / (D / 16), c = i % (D / 16);
+      cp_async16(rk + t * D + ((c ^ (t % (D / 16))) * 16), gk + i * 16);
+    }
     const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
     for (int i = tid; i < nt * (3 * D / 8) / 4; i += kAttnThreads2) cp_async4(rv + i * 4, gv + i * 4);
     const float* gs = a.v_scales + (long long)h * a.T + t0;
@@ -195,11 +203,13 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
     cp_async_wait_all();
     __syncthreads();  // raw tile landed; previous tile's Ks / Ys / Ps are consumed
     // ---- K tile -> Ks[d][t] (f32 dequant); 8 lanes read one token's 128 B ----
+    // (consecutive threads take consecutive tokens: the transposed stores
+    // Ks[d][t] are bank-conflict free; the swizzled raw rows keep the loads so)
     for (int i = tid; i < TT2 * (D / 16); i += kAttnThreads2) {
-      const int t = i / (D / 16), d0 = (i % (D / 16)) * 16;
+      const int t = i % TT2, d0 = (i / TT2) * 16;
       float kv[16];
       if (t < nt) {
-        const uint4 w = *reinterpret_cast<const uint4*>(rk + t * D + d0);
+        const uint4 w = *reinterpret_cast<const uint4*>(rk + t * D + (((d0 >> 4) ^ (t % (D / 16))) * 16));
         const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
         const float s = a.k_mode == PKV_K_TENSOR ? ts
                                                  : __half2float(a.k_bscale[(((long long)h * a.T + t0 + t) * D + d0) >> 5]);
@@ -317,22 +327,27 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
   }
 }
 
-// One warp per (row, kv head): merge tiles, inverse-rotate, add the tail.
+// One CTA of kCombineWarps warps per (row, kv head): the warps merge
+// interleaved subsets of the splits, warp 0 folds their results, then
+// inverse-rotates and adds the private tail.
+constexpr int kCombineWarps = 4;
 template <int D>
-__global__ void combine_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __grid_constant__ Args a) {
   constexpr int EPL = D / 32;  // coordinates per lane: lane holds [EPL*lane, EPL*lane+EPL)
-  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ float s_acc[kCombineWarps][D];
+  __shared__ float s_ml[kCombineWarps][2];
+  const int wid = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp_global >= a.rows * a.kv_heads) return;
-  const int row = warp_global / a.kv_heads;
-  const int h = warp_global % a.kv_heads;
+  const int row = blockIdx.x / a.kv_heads;
+  const int h = blockIdx.x % a.kv_heads;
   const int agent = row / a.group, g = row % a.group;
 
   const long long stride = (long long)a.rows * (D + 4);  // between splits
   const float* base = a.part + ((long long)h * a.splits * a.rows + row) * (D + 4);
-  // split maxima: lanes in parallel over splits
+  // this warp's split maxima: lanes in parallel over its splits
   float M = -INFINITY;
-  for (int sidx = lane; sidx < a.splits; sidx += 32) M = fmaxf(M, base[sidx * stride + D]);
+  for (int sidx = wid + kCombineWarps * lane; sidx < a.splits; sidx += 32 * kCombineWarps)
+    M = fmaxf(M, base[sidx * stride + D]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float L = 0.f;
@@ -340,7 +355,7 @@ __global__ void combine_kernel(const __grid_constant__ Args a) {
 #pragma unroll
   for (int j = 0; j < EPL; ++j) acc[j] = 0.f;
 #pragma unroll 4
-  for (int sidx = 0; sidx < a.splits; ++sidx) {
+  for (int sidx = wid; sidx < a.splits; sidx += kCombineWarps) {
     const float* src = base + sidx * stride;
     const float w = exp2f(src[D] - M);
     L += w * src[D + 1];
@@ -354,6 +369,31 @@ __global__ void combine_kernel(const __grid_constant__ Args a) {
     }
 #pragma unroll
     for (int j = 0; j < EPL; ++j) acc[j] = fmaf(w, v[j], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) s_acc[wid][EPL * lane + j] = acc[j];
+  if (lane == 0) {
+    s_ml[wid][0] = M;
+    s_ml[wid][1] = L;
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  {
+    float Mg = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kCombineWarps; ++w) Mg = fmaxf(Mg, s_ml[w][0]);
+    L = 0.f;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int w = 0; w < kCombineWarps; ++w) {
+      const float mw = s_ml[w][0];
+      const float c = mw == -INFINITY ? 0.f : exp2f(mw - Mg);  // a warp without splits contributes nothing
+      L = fmaf(c, s_ml[w][1], L);
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) acc[j] = fmaf(c, s_acc[w][EPL * lane + j], acc[j]);
+    }
+    M = Mg;
   }
   // inverse rotation of the merged rotated-domain accumulator:
   // in-lane stages over the low log2(EPL) bits, shuffles over the lane bits
@@ -443,8 +483,7 @@ int launch_rt(Args& a, cudaStream_t st) {
   dim3 grid(a.splits, a.kv_heads, row_tiles);
   prefix_kernel2<D, RTILE><<<grid, kAttnThreads2, AT::SMEM, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
-  const int warps = a.rows * a.kv_heads;
-  combine_kernel<D><<<(warps + 7) / 8, 256, 0, st>>>(a);
+  combine_kernel<D><<<a.rows * a.kv_heads, 32 * kCombineWarps, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
 

@@ -1104,11 +1104,10 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     (&ctl->gcnt[0][0])[threadIdx.x] = 0;
   }
   __syncthreads();
-  // Role split. SMs that share instruction caches (same TPC / GPC) should run
-  // the same code path, so the key role takes a contiguous range of SM ids
-  // (the grid is one CTA per SM: %smid is a permutation of 0..grid-1).
-  // Ranks are dense within each role.
-  const unsigned gk = gridDim.x - (unsigned)a.value_ctas;
+  // Role split. SMs that share instruction caches (neighbouring SMs) should
+  // run the same code path, so each role takes a contiguous range of blocks
+  // (PKV_ROLE_MAP=1: of SM ids; the grid is one CTA per SM, so %smid is a
+  // permutation of 0..grid-1). Ranks are dense within each role.
   unsigned pos = blockIdx.x;
 #if PKV_ROLE_MAP == 1
   asm volatile("mov.u32 %0, %%smid;" : "=r"(pos));
