@@ -157,6 +157,7 @@ struct DecArgs {
   int num_layers, head_dim, k_mode, out_bytes;
   long long nvec, nelem;
   int nK, nV;
+  int key_ctas;  // > 0: CTAs [grid - key_ctas, grid) decode keys, the rest values; 0: interleaved items
   unsigned int total;
   float sqrt_d32, rcp_sqrt_d32;
   uint32_t sign_bits[8];
@@ -1299,12 +1300,26 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
     if (lane == 0) {
       const uint64_t pol_first = tma::policy_evict_first();
       // static slice of the item list per CTA; within the CTA items go to
-      // whichever group frees a stage first
-      unsigned long long t = blockIdx.x;
+      // whichever group frees a stage first. With a role split (key_ctas >
+      // 0) each SM runs one code path: key CTAs stream the (HBM-bound) key
+      // items of every layer, value CTAs the (ALU-bound) value items, and
+      // the two overlap instead of alternating on every SM.
+      const int vctas = a.key_ctas > 0 ? (int)gridDim.x - a.key_ctas : (int)gridDim.x;
+      const bool key_role = a.key_ctas > 0 && (int)blockIdx.x >= vctas;
+      const long long G = a.key_ctas > 0 ? (key_role ? a.key_ctas : vctas) : (long long)gridDim.x;
+      const long long per = key_role ? a.nK : a.nV;
+      const long long total = a.key_ctas > 0 ? (long long)a.num_layers * per : (long long)a.total;
+      long long t = key_role ? (long long)blockIdx.x - vctas : (long long)blockIdx.x;
       auto next_item = [&]() -> Item {
-        if (t >= a.total) return Item{kEnd, 0, 0, 0};
-        const Item it = dec_item(a, (unsigned int)t);
-        t += gridDim.x;
+        if (t >= total) return Item{kEnd, 0, 0, 0};
+        Item it;
+        if (a.key_ctas > 0) {
+          const int l = (int)(t / per);
+          it = Item{key_role ? kKeyDec : kValDec, l, (int)(t - (long long)l * per), 0};
+        } else {
+          it = dec_item(a, (unsigned int)t);
+        }
+        t += G;
         return it;
       };
       auto issue = [&](const Item& it, uint8_t* in, uint64_t* bar) {
@@ -1593,7 +1608,9 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // block32 (one key pass) 0.36 -> 336, 0.4 -> 302, 0.43 -> 285. The curve is not
       // smooth: SMs sharing instruction caches should run one role, so
       // where the role boundary falls matters. PKV_KEY_SM_FRACTION overrides
-      double frac = r.k_mode == PKV_K_TENSOR ? 0.38 : 0.43;
+      // (d64, whose value path is cheaper: C2 0.35 -> 188 us, 0.42 -> 169, 0.46 -> 178)
+      const bool d128 = r.head_dim >= 128;
+      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? 0.38 : 0.42) : (d128 ? 0.43 : 0.46);
       if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
       key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
     } else if (do_k) {
@@ -1638,6 +1655,17 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
     return PKV_ERR_INVALID_ARG;
   }
   a->total = (unsigned int)total;
+  a->key_ctas = 0;
+  if (do_k && do_v) {
+    // share of SMs for the key role, swept with tools/dec_frac.sh: C3 (d128)
+    // 0 (interleaved items) -> 180 us, 0.3 -> 164, 0.35 -> 140, 0.39 -> 147;
+    // C2 (d64, cheaper value path) 0 -> 109 us, 0.35 -> 96, 0.4 -> 89, 0.45 -> 97.
+    // PKV_DEC_KEY_FRACTION overrides (0 = interleaved items on every SM)
+    double frac = r.head_dim >= 128 ? 0.35 : 0.4;
+    if (const char* f = std::getenv("PKV_DEC_KEY_FRACTION")) frac = std::atof(f);
+    const int grid = sm_count();
+    if (frac > 0.0) a->key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
+  }
   int rc = PKV_OK;
   for (int l = 0; l < L && rc == PKV_OK; ++l) {
     if (do_k) {
