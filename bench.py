@@ -404,8 +404,8 @@ def run_ours(args, cfg):
     kb = 4 if args.k_mode == "tensor" else 2 * ((n + 31) // 32)
     bytes_k = L * (n * in_b + n + kb)                      # key encode (absmax pass + codes)
     bytes_v = L * (n * in_b + 3 * n / 8 + 4 * vecs)        # value encode
-    kernels = {"encode_values": (enc_v_ms, bytes_v), "encode_keys": (enc_k_ms, bytes_k),
-               "decode": (dec_ms, deq_b)}
+    # the step's two launches: the fused encode (value + key roles) and the decode
+    kernels = {"encode": (enc_ms, comp_b), "decode": (dec_ms, deq_b)}
     dom_name = max(kernels, key=lambda k: kernels[k][0])
     dom_ms, dom_bytes = kernels[dom_name]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
