@@ -1170,10 +1170,17 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         // consumer ever holds a stage waiting for a scale; while layer l is
         // not ready the producer issues absmax items instead, at most `lag`
         // layers ahead of the encode cursor (L2 footprint).
-        const long long G = (long long)gridDim.x - a.value_ctas;
-        const long long totA = (long long)a.num_layers * a.nA, totE = (long long)a.num_layers * a.nE;
-        long long ta = role_rank, te = role_rank;
+        // (32-bit cursors: the host caps a launch at 2^31 items; the layer
+        // count of the encode cursor is polled without blocking: the load
+        // issued at one call is consumed at the next, so its L2 round trip
+        // overlaps the TMA issue in between)
+        const uint32_t G = gridDim.x - (uint32_t)a.value_ctas;
+        const uint32_t nA = (uint32_t)a.nA, nE = (uint32_t)a.nE;
+        const uint32_t totA = (uint32_t)a.num_layers * nA, totE = (uint32_t)a.num_layers * nE;
+        uint32_t ta = (uint32_t)role_rank, te = (uint32_t)role_rank;
         int ready = -1;  // layers [0, ready] staged in ctl->layer_max
+        int polled = -1;     // layer whose count is in `polled_cnt`
+        uint32_t polled_cnt = 0;
         auto stage = [&](int l) {
           ctl->layer_max[l] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + l);
           __threadfence_block();
@@ -1183,25 +1190,27 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         auto next_item = [&]() -> Item {
           for (;;) {
             if (te >= totE) return Item{kEnd, 0, 0, 0};
-            const int el = (int)(te / a.nE);
+            const int el = (int)(te / nE);
             if (el <= ready) {
-              const Item it{kKeyEnc, el, (int)(te - (long long)el * a.nE), 0};
+              const Item it{kKeyEnc, el, (int)(te - (uint32_t)el * nE), 0};
               te += G;
               return it;
             }
-            if (ld_acquire_u32(a.layer_done + el) >= (uint32_t)a.nA) {
+            if (polled == el && polled_cnt >= nA) {
               stage(el);
               continue;
             }
-            if (ta < totA && ta / a.nA < (long long)el + a.key_lag) {
-              const int al = (int)(ta / a.nA);
-              const Item it{kAbsmax, al, (int)(ta - (long long)al * a.nA), 0};
+            polled = el;
+            polled_cnt = ld_acquire_u32(a.layer_done + el);  // consumed at the next call
+            if (ta < totA && (int)(ta / nA) < el + a.key_lag) {
+              const int al = (int)(ta / nA);
+              const Item it{kAbsmax, al, (int)(ta - (uint32_t)al * nA), 0};
               ta += G;
               return it;
             }
             uint32_t spins = 0;
             uint64_t t0 = 0;
-            while (ld_acquire_u32(a.layer_done + el) < (uint32_t)a.nA) {
+            while (ld_acquire_u32(a.layer_done + el) < nA) {
               __nanosleep(128);
               tma::watchdog(spins, t0);
             }
