@@ -1621,7 +1621,10 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       const bool d128 = r.head_dim >= 128;
       double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? 0.38 : 0.42) : (d128 ? 0.43 : 0.46);
       if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
-      key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
+      // an even count: the two SMs of a TPC must run the same role (an odd
+      // split puts both code paths on one TPC, which thrashes and, with the
+      // static partition, stalls the whole role: 53 key CTAs 290 us vs 52: 267)
+      key_ctas = std::max(2, std::min(grid - 2, 2 * (int)std::lround(frac * grid / 2.0)));
     } else if (do_k) {
       key_ctas = grid;
     }
@@ -1670,10 +1673,10 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
     // 0 (interleaved items) -> 180 us, 0.3 -> 164, 0.35 -> 140, 0.39 -> 147;
     // C2 (d64, cheaper value path) 0 -> 109 us, 0.35 -> 96, 0.4 -> 89, 0.45 -> 97.
     // PKV_DEC_KEY_FRACTION overrides (0 = interleaved items on every SM)
-    double frac = r.head_dim >= 128 ? 0.35 : 0.4;
+    double frac = r.head_dim >= 128 ? 0.35 : 0.39;  // (C2 with even counts: 0.378 -> 90.3, 0.392 -> 88.6, 0.405 -> 91.0)
     if (const char* f = std::getenv("PKV_DEC_KEY_FRACTION")) frac = std::atof(f);
     const int grid = sm_count();
-    if (frac > 0.0) a->key_ctas = std::max(1, std::min(grid - 1, (int)std::lround(frac * grid)));
+    if (frac > 0.0) a->key_ctas = std::max(2, std::min(grid - 2, 2 * (int)std::lround(frac * grid / 2.0)));  // even: whole TPCs
   }
   int rc = PKV_OK;
   for (int l = 0; l < L && rc == PKV_OK; ++l) {
