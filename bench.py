@@ -333,11 +333,21 @@ def run_ours(args, cfg):
         host_out = [(torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory(),
                      torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in range(L)]
 
+        inflight = []
+
         def e2e_step():
             # build_pool uploads the pinned dump chunk by chunk, overlapped with
-            # the encode; materialize_to_host overlaps decode with the D2H copies
+            # the encode; materialize_to_host overlaps decode with the D2H copies.
+            # The host may run one step ahead (step n+1 uploads while step n
+            # downloads) but no further: unbounded run-ahead makes the caching
+            # allocator grow (cudaMalloc stalls the host for 100s of ms).
             p = pk.build_pool(host_dump, build_stats=False, device=dev, check=False)
             p.attach(16).materialize_to_host(host_out)
+            done = torch.cuda.Event()
+            done.record(stream)
+            inflight.append(done)
+            if len(inflight) > 1:
+                inflight.pop(0).synchronize()
 
         # warm the caching allocator (each step allocates a fresh pool and
         # staging buffers; the first steps pay cudaMalloc) before timing
