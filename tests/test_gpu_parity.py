@@ -354,3 +354,29 @@ def test_random_shapes_tails_and_modes_bit_exact(seed):
             assert np.array_equal(u32(vq.scales), vs.view(np.uint32))
             assert np.array_equal(u32(dec[li][0]), kd.view(np.uint32)), (li, bits)
             assert np.array_equal(u32(dec[li][1]), vd.view(np.uint32)), (li, bits)
+
+
+@pytest.mark.parametrize("mode", ["tensor", "block32"])
+def test_role_splits_and_schedules_do_not_change_results(monkeypatch, mode):
+    # the encode / decode work split between key and value CTAs, the absmax
+    # lag and the interleaved-decode fallback are scheduling knobs only:
+    # every setting must give bit-identical pools and decoded tensors
+    g = pk.ModelGeometry(num_layers=9, kv_heads=4, head_dim=128, seq_len=700)
+    dump = pk.synth_gaussian_dump(g, seed=11, device="cuda", dtype=torch.bfloat16, generator="torch")
+    ref = pk.build_pool(dump, k_scale_mode=mode)
+    ref_out = ref.attach(16).materialize_all()
+    for enc_frac, dec_frac, lag in [("0.1", "0.1", "1"), ("0.6", "0", "2"), ("0.9", "0.9", "8")]:
+        monkeypatch.setenv("PKV_KEY_SM_FRACTION", enc_frac)
+        monkeypatch.setenv("PKV_DEC_KEY_FRACTION", dec_frac)
+        monkeypatch.setenv("PKV_KEY_LAG", lag)
+        p = pk.build_pool(dump, k_scale_mode=mode)
+        for i in range(g.num_layers):
+            (ka, va), (kb, vb) = ref.layer_blocks(i), p.layer_blocks(i)
+            assert torch.equal(ka.codes, kb.codes) and torch.equal(va.packed, vb.packed)
+            assert torch.equal(va.scales, vb.scales)
+            if mode == "tensor":
+                assert ka.scale == kb.scale
+            else:
+                assert torch.equal(ka.block_scales, kb.block_scales)
+        for (k0, v0), (k1, v1) in zip(ref_out, p.attach(16).materialize_all()):
+            assert torch.equal(k0, k1) and torch.equal(v0, v1)
