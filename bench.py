@@ -317,10 +317,14 @@ def run_ours(args, cfg):
 
     enc_k_ms = time_it(run_enc_k, args.steps)
     enc_v_ms = time_it(run_enc_v, args.steps)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        return float(t.item())
+
+    total_ms = max_over_ranks(total_ms)
     ms_step = total_ms / args.steps
     comp_b, deq_b = algorithmic_bytes(L, H, D, T, in_b, 2, args.k_mode)
     value = world * (comp_b + deq_b) / (ms_step / 1e3) / 1e9
@@ -356,12 +360,14 @@ def run_ours(args, cfg):
         torch.cuda.synchronize(dev)
         es, ee = ev(), ev()
         n_e2e = max(3, min(args.steps, 20))
+        if world > 1:
+            dist.barrier()
         es.record(stream)
         for _ in range(n_e2e):
             e2e_step()
         ee.record(stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = es.elapsed_time(ee) / n_e2e
+        e2e_ms = max_over_ranks(es.elapsed_time(ee) / n_e2e)
         h2d = 2 * L * g.elements_per_tensor * in_b
         d2h = 2 * L * g.elements_per_tensor * 2
         e2e = {"value": world * (comp_b + deq_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
@@ -383,12 +389,14 @@ def run_ours(args, cfg):
             attn_step()
         torch.cuda.synchronize(dev)
         s2, e2 = ev(), ev()
+        if world > 1:
+            dist.barrier()
         s2.record(stream)
         for _ in range(args.steps):
             attn_step()
         e2.record(stream)
         torch.cuda.synchronize(dev)
-        a_ms = s2.elapsed_time(e2) / args.steps
+        a_ms = max_over_ranks(s2.elapsed_time(e2) / args.steps)
         pool_bytes = L * (g.elements_per_tensor * (1 + 3 / 8) + 4 * g.vectors_per_tensor + 4)
         attn = {"tokens_per_s": world * agents / (a_ms / 1e3), "ms_per_token_step": a_ms,
                 "agents": agents, "layers": L, "scope": "attention only (all layers), batched agents",
