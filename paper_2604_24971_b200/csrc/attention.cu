@@ -347,31 +347,53 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
 
   const long long stride = (long long)a.rows * (D + 4);  // between splits
   const float* base = a.part + ((long long)h * a.splits * a.rows + row) * (D + 4);
-  // this warp's split maxima: lanes in parallel over its splits
-  float M = -INFINITY;
-  for (int sidx = wid + kCombineWarps * lane; sidx < a.splits; sidx += 32 * kCombineWarps)
-    M = fmaxf(M, base[sidx * stride + D]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float L = 0.f;
+  // this warp's splits (wid, wid + W, ...), CH at a time: the CH partials'
+  // loads are all issued before any is used (one L2 round trip per chunk),
+  // then folded with an online max
+  constexpr int CH = 8;
+  float M = -INFINITY, L = 0.f;
   float acc[EPL];
 #pragma unroll
   for (int j = 0; j < EPL; ++j) acc[j] = 0.f;
-#pragma unroll 4
-  for (int sidx = wid; sidx < a.splits; sidx += kCombineWarps) {
-    const float* src = base + sidx * stride;
-    const float w = exp2f(src[D] - M);
-    L += w * src[D + 1];
-    float v[EPL];
-    if constexpr (EPL == 4) {
-      const float4 t = *reinterpret_cast<const float4*>(src + 4 * lane);
-      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    } else {
+  for (int s0 = wid; s0 < a.splits; s0 += kCombineWarps * CH) {
+    float mv[CH], lv[CH], vv[CH][EPL];
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) v[j] = src[EPL * lane + j];
+    for (int c = 0; c < CH; ++c) {
+      const int sidx = s0 + c * kCombineWarps;
+      if (sidx < a.splits) {
+        const float* src = base + sidx * stride;
+        mv[c] = src[D];
+        lv[c] = src[D + 1];
+        if constexpr (EPL == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(src + 4 * lane);
+          vv[c][0] = t.x; vv[c][1] = t.y; vv[c][2] = t.z; vv[c][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) vv[c][j] = src[EPL * lane + j];
+        }
+      } else {
+        mv[c] = -INFINITY;
+        lv[c] = 0.f;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) vv[c][j] = 0.f;
+      }
     }
+    float mc = M;
 #pragma unroll
-    for (int j = 0; j < EPL; ++j) acc[j] = fmaf(w, v[j], acc[j]);
+    for (int c = 0; c < CH; ++c) mc = fmaxf(mc, mv[c]);
+    if (mc == -INFINITY) continue;  // no tokens in these splits
+    const float r = exp2f(M - mc);   // M = -inf: 0 (acc and L are 0 then)
+    L *= r;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) acc[j] *= r;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const float w = exp2f(mv[c] - mc);  // an empty split (-inf) weighs 0
+      L = fmaf(w, lv[c], L);
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) acc[j] = fmaf(w, vv[c][j], acc[j]);
+    }
+    M = mc;
   }
 #pragma unroll
   for (int j = 0; j < EPL; ++j) s_acc[wid][EPL * lane + j] = acc[j];
