@@ -9,7 +9,8 @@
 // Layout of the work:
 //   * all agents' query rows that share a KV head (rows = agents * group) are
 //     processed together, so each pool tile is read from HBM once per step;
-//   * the prefix is cut into ~2 splits per SM, one CTA per (kv head, split,
+//   * the prefix is cut into whole-tile splits, ~2 CTAs per SM (8 for
+//     16-row tiles at d=64), one CTA per (kv head, split,
 //     64-row tile); a CTA walks its split in 64-token tiles, converting each
 //     K tile (int8 codes * scale, exactly the reference dequant) to f32 in
 //     shared memory and each V tile to the *rotated* domain
@@ -21,6 +22,7 @@
 //     tail (tokens appended after the shared prefix).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/polykv.h"
@@ -134,7 +136,9 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
   const int h = blockIdx.y;
   const int sp = blockIdx.x;
   const int r0 = blockIdx.z * RT;
-  const long long per = (a.T + a.splits - 1) / a.splits;
+  // splits start on tile boundaries (whole tiles per split, see attn_splits)
+  const long long tiles = (a.T + TT2 - 1) / TT2;
+  const long long per = (tiles + a.splits - 1) / a.splits * TT2;
   const long long t_begin = (long long)sp * per, t_end = min(a.T, t_begin + per);
   const int tid = threadIdx.x;
   const int rg = tid >> 4, cg = tid & 15;  // row group, column (token / d) group
@@ -487,15 +491,32 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
   }
 }
 
-// splits per head: about two CTAs per SM (two co-resident CTAs hide each
-// other's tile loads), each split at least one tile
-inline int attn_splits(int kv_heads, long long T, int row_tiles) {
+// splits per head: about `per_sm` CTAs per SM (co-resident CTAs hide each
+// other's tile loads), each split at least one tile. 64-row tiles fit two
+// CTAs per SM (shared memory); the 16-row tile (rows <= 16) fits more at d=64.
+// PKV_ATTN_CTAS_PER_SM overrides (tuning only).
+#ifndef PKV_ATTN_SMALL_PER_SM
+#define PKV_ATTN_SMALL_PER_SM 8  // d=64 (C2, 5 rows per head): 0.58 -> 0.49 ms per 24-layer step vs 2
+#endif
+inline int attn_splits(int kv_heads, long long T, int rows, int head_dim) {
+  static const int env_per_sm = [] {
+    const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int rt = rows <= 16 ? 16 : 64;
+  const int row_tiles = (rows + rt - 1) / rt;
+  const int per_sm = env_per_sm > 0 ? env_per_sm : (rt == 16 && head_dim == 64 ? PKV_ATTN_SMALL_PER_SM : 2);
+  // (16-row tiles at d=128 fill shared memory at two CTAs per SM as well)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long want = (2LL * sms + (long long)kv_heads * row_tiles - 1) / ((long long)kv_heads * row_tiles);
-  const long long max_splits = (T + TT2 - 1) / TT2;
-  return (int)std::max(1LL, std::min(want, max_splits));
+  const long long den = (long long)kv_heads * row_tiles;
+  const long long want = std::max(1LL, ((long long)per_sm * sms + den - 1) / den);
+  // whole tiles per split (a ragged split costs a full tile step), then the
+  // fewest splits of that length
+  const long long tiles = (T + TT2 - 1) / TT2;
+  const long long per = (tiles + want - 1) / want;
+  return (int)((tiles + per - 1) / per);
 }
 
 template <int D, int RTILE>
@@ -526,7 +547,7 @@ size_t pkv_attention_workspace_bytes(int num_rows, int kv_heads, int group, int 
                                      int64_t seq_len) {
   if (num_rows < 1 || kv_heads < 1 || group < 1 || head_dim < 1 || seq_len < 1) return 0;
   const int rows = num_rows * group;
-  const int splits = pkv::attn::attn_splits(kv_heads, seq_len, (rows + (rows <= 16 ? 15 : 63)) / (rows <= 16 ? 16 : 64));
+  const int splits = pkv::attn::attn_splits(kv_heads, seq_len, rows, head_dim);
   return sizeof(float) * (size_t)kv_heads * (size_t)splits * (size_t)rows * (size_t)(head_dim + 4);
 }
 
@@ -563,10 +584,7 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, in
   a.q_dtype = q_dtype;
   a.out_dtype = out_dtype;
   a.k_mode = k_mode;
-  {
-    const int rt = a.rows <= 16 ? 16 : 64;
-    a.splits = attn_splits(kv_heads, seq_len, (a.rows + rt - 1) / rt);
-  }
+  a.splits = attn_splits(kv_heads, seq_len, a.rows, head_dim);
   a.qscale = softmax_scale * kLog2e;
   for (int i = 0; i < 8; ++i) a.cent32[i] = (float)centroids_host[i];
   if (sign_bits_host) {

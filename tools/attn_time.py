@@ -7,6 +7,8 @@ from paper_2604_24971_b200.attention import decode_attention
 L, H, D, T, A, G = 32, 8, 128, 4096, 15, 4
 if len(sys.argv) > 1 and sys.argv[1] == "c2":
     L, H, D, T, A, G = 24, 32, 64, 1851, 5, 1
+if len(sys.argv) > 2:  # agent count override (e.g. few agents: 16-row tiles)
+    A = int(sys.argv[2])
 dev = torch.device("cuda")
 g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
 pool = pk.build_pool(pk.synth_gaussian_dump(g, seed=0, device=dev, dtype=torch.bfloat16, generator="torch"))
