@@ -216,23 +216,31 @@ def test_packed_snapshot_roundtrip(tmp_path, golden):
             assert torch.equal(k1, k2) and torch.equal(v1, v2)
 
 
-def test_decode_attention_matches_fp64_oracle():
+# (kv_heads, head_dim, seq_len, agents, group): 64-row tiles with ragged T,
+# 16-row tiles at d=64 (8 CTAs per SM: many one-tile splits, T < one tile,
+# T one token past a tile) and at d=128
+ATTN_SHAPES = [(8, 128, 1000, 15, 4), (32, 64, 1851, 5, 1), (32, 64, 40, 3, 1), (4, 64, 4097, 16, 1),
+               (8, 128, 700, 2, 4), (2, 128, 65, 1, 4)]
+
+
+@pytest.mark.parametrize("shape", ATTN_SHAPES, ids=lambda s: "h%d_d%d_t%d_a%d_g%d" % s)
+def test_decode_attention_matches_fp64_oracle(shape):
     from paper_2604_24971_b200 import attention as A
 
-    g = pk.ModelGeometry(num_layers=1, kv_heads=8, head_dim=128, seq_len=1000)
+    H, D, T, R, G = shape
+    g = pk.ModelGeometry(num_layers=1, kv_heads=H, head_dim=D, seq_len=T)
     dump = pk.synth_gaussian_dump(g, seed=3, device="cuda")
     pool = pk.build_pool(dump, build_stats=False)
-    R, G = 15, 4
-    q = torch.randn(R, 8, G, 128, device="cuda")
+    q = torch.randn(R, H, G, D, device="cuda")
     tail_len = torch.randint(0, 9, (R,), device="cuda", dtype=torch.int32)
-    tk = torch.randn(R, 8, 8, 128, device="cuda").bfloat16()
-    tv = torch.randn(R, 8, 8, 128, device="cuda").bfloat16()
+    tk = torch.randn(R, H, 8, D, device="cuda").bfloat16()
+    tv = torch.randn(R, H, 8, D, device="cuda").bfloat16()
     out = A.decode_attention(pool, 0, q, tail_k=tk, tail_v=tv, tail_len=tail_len,
-                             softmax_scale=128 ** -0.5, out_dtype=torch.float32)
+                             softmax_scale=D ** -0.5, out_dtype=torch.float32)
     (kd, vd), = pool.decode_layers([0], torch.float32)
     tails_k = [tk[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
     tails_v = [tv[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
-    want = O.attention_over_pool(q.cpu().numpy(), kd[0].cpu().numpy(), vd[0].cpu().numpy(), 128 ** -0.5,
+    want = O.attention_over_pool(q.cpu().numpy(), kd[0].cpu().numpy(), vd[0].cpu().numpy(), D ** -0.5,
                                  tails_k, tails_v)
     got = out.cpu().numpy().astype(np.float64)
     rel = np.abs(got - want).max() / np.abs(want).max()
