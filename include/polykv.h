@@ -58,6 +58,7 @@ extern "C" {
 #define PKV_FLAG_K_NONFINITE 0x1u
 #define PKV_FLAG_V_NONFINITE 0x2u
 #define PKV_FLAG_K_SCALE_OVERFLOW 0x4u
+#define PKV_FLAG_BAD_CODE 0x8u /* pkv_pack_codes: a code > 7 (CorruptBlockError) */
 
 /* Maximum layers handled by one kernel launch; larger pools are processed
  * in consecutive launches by the same call. */
@@ -65,6 +66,12 @@ extern "C" {
 
 int pkv_abi_version(void);
 const char* pkv_status_string(int status);
+
+/* Scheduling knobs (PKV_KEY_SM_FRACTION, PKV_DEC_KEY_FRACTION, PKV_KEY_LAG,
+ * PKV_ATTN_CTAS_PER_SM, PKV_CODEC_PATH, PKV_DBG_ENC) are
+ * read from the environment once, at the first launch, not per call. This
+ * re-reads them (for A/B tuning in one process). None changes a result. */
+int pkv_reload_tuning(void);
 
 /* Head dims supported by the value kernels: 8, 16, 32, 64, 128, 256.
  * Key kernels accept any head_dim. Returns 1 if supported. */
@@ -125,7 +132,7 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
                void* const* k_out, void* const* v_out, void* stream);
 
 /* Canonical uint8 codes <-> packed 3-bit payload over `count` codes
- * (valuequant.py:312-345). pkv_pack_codes ORs PKV_FLAG bit 0x8 into
+ * (valuequant.py:312-345). pkv_pack_codes ORs PKV_FLAG_BAD_CODE into
  * *bad_code (device uint32) when a code exceeds 7. */
 int pkv_unpack_codes(const uint8_t* packed, int64_t count, uint8_t* codes,
                      void* stream);

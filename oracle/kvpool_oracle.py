@@ -63,19 +63,20 @@ def fwht_last_axis(arr: np.ndarray) -> np.ndarray:
     fwht.py:24-41: stages half = 1, 2, 4, ...; at each stage the pair
     (lo, hi) = (x[i], x[i + half]) becomes (lo + hi, lo - hi).
     """
-    x = np.array(arr, copy=True)
+    x = np.array(arr, copy=True, order="C")
     d = x.shape[-1]
     if d < 1 or d & (d - 1):
         raise ValueError(f"transform length must be a power of two, got {d}")
-    idx = np.arange(d)
+    lead = x.shape[:-1]
     h = 1
     while h < d:
-        lo = idx[(idx & h) == 0]
-        hi = lo + h
-        a = x[..., lo]
-        b = x[..., hi]
-        x[..., lo] = a + b
-        x[..., hi] = a - b
+        # coordinate i = (block, bit h of i, offset): lo = bit clear, hi = set
+        view = x.reshape(lead + (d // (2 * h), 2, h))
+        a = view[..., 0, :]
+        b = view[..., 1, :]
+        s, t = a + b, a - b
+        view[..., 0, :] = s
+        view[..., 1, :] = t
         h <<= 1
     return x
 

@@ -39,6 +39,7 @@ P = ctypes.POINTER
 SIGNATURES: dict[str, tuple] = {
     "pkv_abi_version": (c_int, []),
     "pkv_status_string": (ctypes.c_char_p, [c_int]),
+    "pkv_reload_tuning": (c_int, []),
     "pkv_v_head_dim_supported": (c_int, [c_int]),
     "pkv_encode_workspace_bytes": (c_size, [c_int, c_i64, c_int]),
     "pkv_encode": (
@@ -99,6 +100,12 @@ def load() -> ctypes.CDLL:
             fn.argtypes = args
         _lib = lib
         return lib
+
+
+def reload_tuning() -> None:
+    """Re-read the PKV_* scheduling knobs from os.environ (they are otherwise
+    read once per process; see include/polykv.h pkv_reload_tuning)."""
+    load().pkv_reload_tuning()
 
 
 def check(status: int, what: str) -> None:

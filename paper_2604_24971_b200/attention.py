@@ -7,7 +7,6 @@ private bf16 tail (tokens generated after the shared prefix).
 
 from __future__ import annotations
 
-import numpy as np
 import torch
 
 from . import _codec
@@ -49,10 +48,19 @@ def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: t
     if tail_len is not None:
         if tail_k is None or tail_v is None:
             raise ValueError("tail_len needs tail_k and tail_v")
+        if tail_k.dim() != 4 or tuple(tail_k.shape[:2]) != (R, H) or tail_k.shape[3] != D:
+            raise ValueError(f"tail_k shape {tuple(tail_k.shape)} is not [{R}, {H}, cap, {D}]")
+        if tail_v.shape != tail_k.shape:
+            raise ValueError(f"tail_v shape {tuple(tail_v.shape)} != tail_k shape {tuple(tail_k.shape)}")
+        if tail_len.numel() != R:
+            raise ValueError(f"tail_len has {tail_len.numel()} entries for {R} agents")
+        for t in (tail_k, tail_v, tail_len):
+            if t.device != dev:
+                raise ValueError(f"tail tensors must be on {dev}, got {t.device}")
         tail_k = tail_k.to(torch.bfloat16).contiguous()
         tail_v = tail_v.to(torch.bfloat16).contiguous()
-        tail_len = tail_len.to(device=dev, dtype=torch.int32).contiguous()
-        cap = tail_k.shape[2]
+        tail_len = tail_len.to(dtype=torch.int32).contiguous()
+        cap = tail_k.shape[2]  # the kernel clamps tail_len[r] to cap
     else:
         cap = 0
     scale = float(softmax_scale if softmax_scale is not None else D ** -0.5)
@@ -70,5 +78,3 @@ def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: t
     check(rc, "pkv_decode_attention")
     return out
 
-
-_ = np  # noqa: F401

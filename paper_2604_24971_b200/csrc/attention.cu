@@ -27,6 +27,7 @@
 
 #include "../../include/polykv.h"
 #include "pkv_common.cuh"
+#include "tuning.h"
 
 namespace pkv {
 namespace attn {
@@ -453,7 +454,9 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
   }
 
   // private tail (bf16), online-merged in the original domain
-  const int tl = a.tail_len ? a.tail_len[agent] : 0;
+  // clamped: a tail_len past the buffer (e.g. a graph replayed beyond its
+  // capacity) must not read out of bounds
+  const int tl = a.tail_len ? max(0, min(a.tail_len[agent], a.tail_cap)) : 0;
   if (tl > 0) {
     const __nv_bfloat16* tk = static_cast<const __nv_bfloat16*>(a.tail_k);
     const __nv_bfloat16* tv = static_cast<const __nv_bfloat16*>(a.tail_v);
@@ -499,10 +502,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
 #define PKV_ATTN_SMALL_PER_SM 8  // d=64 (C2, 5 rows per head): 0.58 -> 0.49 ms per 24-layer step vs 2
 #endif
 inline int attn_splits(int kv_heads, long long T, int rows, int head_dim) {
-  static const int env_per_sm = [] {
-    const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int env_per_sm = tuning().attn_ctas_per_sm;
   const int rt = rows <= 16 ? 16 : 64;
   const int row_tiles = (rows + rt - 1) / rt;
   const int per_sm = env_per_sm > 0 ? env_per_sm : (rt == 16 && head_dim == 64 ? PKV_ATTN_SMALL_PER_SM : 2);

@@ -35,6 +35,7 @@
 #include "pkv_common.cuh"
 #include "codec_common.cuh"
 #include "stream_codec.h"
+#include "tuning.h"
 
 namespace pkv {
 
@@ -781,7 +782,7 @@ __global__ void pack_kernel(const uint8_t* __restrict__ codes, long long count,
       oob |= c > 7u;
       w |= (c & 7u) << (3 * e);
     }
-    if (oob && bad) atomicOr(bad, 0x8u);
+    if (oob && bad) atomicOr(bad, PKV_FLAG_BAD_CODE);
     packed[3 * g] = (uint8_t)(w & 0xff);
     packed[3 * g + 1] = (uint8_t)((w >> 8) & 0xff);
     packed[3 * g + 2] = (uint8_t)((w >> 16) & 0xff);
@@ -927,10 +928,7 @@ uintptr_t packed_align(int d) {
 
 namespace {
 // PKV_CODEC_PATH=warp forces the warp-granular kernels (debug / A-B timing).
-bool stream_enabled() {
-  const char* e = std::getenv("PKV_CODEC_PATH");
-  return !(e && std::strcmp(e, "warp") == 0);
-}
+bool stream_enabled() { return !tuning().codec_warp; }
 bool stream_fallback(int rc) { return rc == PKV_ERR_ALIGNMENT || rc == PKV_ERR_UNSUPPORTED_HEAD_DIM; }
 }  // namespace
 

@@ -6,7 +6,49 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
 #include "../../include/polykv.h"
+#include "tuning.h"
+
+namespace pkv {
+namespace {
+Tuning read_env() {
+  Tuning t;
+  if (const char* e = std::getenv("PKV_CODEC_PATH")) t.codec_warp = std::strcmp(e, "warp") == 0;
+  if (const char* e = std::getenv("PKV_DBG_ENC")) t.dbg_enc = std::atoi(e);
+  if (const char* e = std::getenv("PKV_KEY_LAG")) t.key_lag = std::atoi(e);
+  if (const char* e = std::getenv("PKV_KEY_SM_FRACTION")) t.key_sm_fraction = std::atof(e);
+  if (const char* e = std::getenv("PKV_DEC_KEY_FRACTION")) t.dec_key_fraction = std::atof(e);
+  if (const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM")) t.attn_ctas_per_sm = std::atoi(e);
+  return t;
+}
+std::mutex g_reload;
+std::atomic<const Tuning*> g_tuning{nullptr};
+}  // namespace
+
+const Tuning& tuning() {
+  const Tuning* t = g_tuning.load(std::memory_order_acquire);
+  if (t) return *t;
+  reload_tuning();
+  return *g_tuning.load(std::memory_order_acquire);
+}
+
+void reload_tuning() {
+  std::lock_guard<std::mutex> lk(g_reload);
+  // snapshots are immutable and never freed: a launch that read the previous
+  // one on another thread keeps a valid reference (reloads are rare)
+  g_tuning.store(new Tuning(read_env()), std::memory_order_release);
+}
+}  // namespace pkv
+
+extern "C" int pkv_reload_tuning(void) {
+  pkv::reload_tuning();
+  return PKV_OK;
+}
 
 namespace {
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;

@@ -167,47 +167,41 @@ __device__ __forceinline__ bool sign_bit(const uint32_t* bits, int i) {
 // n <= 128 eight interleaved accumulators, larger n split at n/2 rounded
 // down to a multiple of 8. This is the reduction order behind
 // np.mean(np.square(rot), axis=-1) in kvpool/valuequant.py:207.
+//
+// np.square rounds every product before the pairwise add, so each square and
+// each add is written with an explicit rounding intrinsic: nvcc would
+// otherwise contract `r += v * v` into one DFMA (a single rounding), which
+// differs from numpy in the last bit for ~1 in 5 vectors and can flip an f32
+// scale that sits on a rounding boundary -- exactly the vectors the replay
+// exists for. tests/test_capi.py checks the SASS of every replay for DFMA.
+__device__ __forceinline__ double sq_rn(double x) { return __dmul_rn(x, x); }
+
+__device__ inline double pairwise_block8(const double* v, int n) {
+  // n >= 8: eight accumulators, then the remainder sequentially
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = sq_rn(v[j]);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq_rn(v[i + j]));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, sq_rn(v[i]));
+  return res;
+}
+
 __device__ inline double pairwise_sumsq(const double* v, int n) {
   if (n < 8) {
     double r = 0.0;
-    for (int i = 0; i < n; ++i) r += v[i] * v[i];
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, sq_rn(v[i]));
     return r;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = v[j] * v[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += v[i + j] * v[i + j];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += v[i] * v[i];
-    return res;
-  }
+  if (n <= 128) return pairwise_block8(v, n);
   int n2 = n / 2;
   n2 -= n2 % 8;
   // depth is at most log2(256/128) = 1 for the supported head dims
-  double a = 0.0, b = 0.0;
-  {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = v[j] * v[j];
-    int i = 8;
-    for (; i < n2 - (n2 % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += v[i + j] * v[i + j];
-    a = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n2; ++i) a += v[i] * v[i];
-  }
-  {
-    const double* w = v + n2;
-    const int m = n - n2;
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = w[j] * w[j];
-    int i = 8;
-    for (; i < m - (m % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] += w[i + j] * w[i + j];
-    b = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < m; ++i) b += w[i] * w[i];
-  }
-  return a + b;
+  return __dadd_rn(pairwise_block8(v, n2), pairwise_block8(v + n2, n - n2));
 }
 
 }  // namespace pkv

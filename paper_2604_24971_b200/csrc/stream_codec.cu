@@ -1073,7 +1073,10 @@ __device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes
     }
     if (!any) {
       __nanosleep(32);
-      tma::watchdog(spins, t0);
+      tma::watchdog(spins, t0);  // traps only after ~10 s without progress
+    } else {
+      spins = 0;
+      t0 = 0;
     }
   }
 }
@@ -1407,6 +1410,7 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
 // host side
 // ===========================================================================
 #include "stream_codec.h"
+#include "tuning.h"
 
 namespace pkv {
 namespace stream {
@@ -1552,7 +1556,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   // workspace: [u32 layer_max L]
   unsigned int* w32 = reinterpret_cast<unsigned int*>(r.ws);
   a->total = (unsigned int)total;
-  if (const char* dbg = std::getenv("PKV_DBG_ENC")) a->dbg = std::atoi(dbg);
+  a->dbg = tuning().dbg_enc;
   a->layer_max = w32;
   const size_t ws_need = workspace_bytes(L, r.num_vectors, r.head_dim);
   if (r.ws_bytes < ws_need) {
@@ -1592,7 +1596,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // lag: enough layers that the key CTAs' in-flight stages (~3 rings per
       // CTA) cannot reach E(l) before every A(l) item has been consumed
       int lag = 4;
-      if (const char* f = std::getenv("PKV_KEY_LAG")) lag = std::max(1, std::atoi(f));
+      if (tuning().key_lag > 0) lag = tuning().key_lag;
       a->key_lag = lag;
       for (int j = 0; j < L + lag; ++j) {
         if (j < L) {
@@ -1620,7 +1624,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // (d64, whose value path is cheaper: C2 0.35 -> 188 us, 0.42 -> 169, 0.46 -> 178)
       const bool d128 = r.head_dim >= 128;
       double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? 0.38 : 0.42) : (d128 ? 0.43 : 0.46);
-      if (const char* f = std::getenv("PKV_KEY_SM_FRACTION")) frac = std::atof(f);
+      if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
       // an even count: the two SMs of a TPC must run the same role (an odd
       // split puts both code paths on one TPC, which thrashes and, with the
       // static partition, stalls the whole role: 53 key CTAs 290 us vs 52: 267)
@@ -1674,7 +1678,7 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
     // C2 (d64, cheaper value path) 0 -> 109 us, 0.35 -> 96, 0.4 -> 89, 0.45 -> 97.
     // PKV_DEC_KEY_FRACTION overrides (0 = interleaved items on every SM)
     double frac = r.head_dim >= 128 ? 0.35 : 0.39;  // (C2 with even counts: 0.378 -> 90.3, 0.392 -> 88.6, 0.405 -> 91.0)
-    if (const char* f = std::getenv("PKV_DEC_KEY_FRACTION")) frac = std::atof(f);
+    if (tuning().dec_key_fraction >= 0.0) frac = tuning().dec_key_fraction;
     const int grid = sm_count();
     if (frac > 0.0) a->key_ctas = std::max(2, std::min(grid - 2, 2 * (int)std::lround(frac * grid / 2.0)));  // even: whole TPCs
   }

@@ -102,12 +102,18 @@ def build_pool_sharded(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_se
     enc = encode_fn or _encode_layers
     ks = [dump.layers[i][0] for i in mine]
     vs = [dump.layers[i][1] for i in mine]
+    if device is None and torch.cuda.is_available():
+        device = torch.device("cuda", torch.cuda.current_device())
     if ks:
         _, _, arena = enc(ks, vs, g, codebook, sign_seed, k_scale_mode, device=device, check=False)
-    else:  # more ranks than layers: contribute an empty slice
+    else:  # more ranks than layers: contribute an empty slice (on the device NCCL gathers from)
         arena = _Arena(g, 0, k_scale_mode, device)
-    raise_for_status(arena.status)  # data faults of this rank's layers, before the collective
     full = gather_arena(arena, g.num_layers, group)
+    # Data faults (non-finite input, fp16 scale overflow) are checked on the
+    # GATHERED status words, so every rank sees every rank's faults and raises
+    # the same exception after the collective; raising before it would leave
+    # the healthy ranks blocked in all_gather.
+    raise_for_status(full.status)
     return pool_from_arena(full, g, codebook, sign_seed, k_scale_mode)
 
 

@@ -11,6 +11,7 @@ import pytest
 import torch
 
 import paper_2604_24971_b200 as pk
+from paper_2604_24971_b200 import _lib
 from oracle import kvpool_oracle as O
 from pkv_testutil import golden_case
 
@@ -377,6 +378,7 @@ def test_role_splits_and_schedules_do_not_change_results(monkeypatch, mode):
         monkeypatch.setenv("PKV_KEY_SM_FRACTION", enc_frac)
         monkeypatch.setenv("PKV_DEC_KEY_FRACTION", dec_frac)
         monkeypatch.setenv("PKV_KEY_LAG", lag)
+        _lib.reload_tuning()  # knobs are read once per process otherwise
         p = pk.build_pool(dump, k_scale_mode=mode)
         for i in range(g.num_layers):
             (ka, va), (kb, vb) = ref.layer_blocks(i), p.layer_blocks(i)
@@ -388,3 +390,5 @@ def test_role_splits_and_schedules_do_not_change_results(monkeypatch, mode):
                 assert torch.equal(ka.block_scales, kb.block_scales)
         for (k0, v0), (k1, v1) in zip(ref_out, p.attach(16).materialize_all()):
             assert torch.equal(k0, k1) and torch.equal(v0, v1)
+    monkeypatch.undo()
+    _lib.reload_tuning()

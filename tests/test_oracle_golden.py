@@ -163,3 +163,26 @@ def test_compression_ratio_is_32_over_11():
     # pkg/tests/test_acceptance.py:57-61
     r = O.compression_ratio_exact(8, 3, 16)
     assert r == Fraction(32, 11) and f"{float(r):.2f}" == "2.91"
+
+
+def test_fma_adversarial_fixture_is_adversarial():
+    """tests/golden/adversarial_fma.npz (make_adversarial.py, from the
+    reference's quantize_v): the oracle reproduces it, and for every vector a
+    sum of squares with r += v*v contracted to one fma rounding gives a
+    different f32 scale than numpy's order (valuequant.py:207)."""
+    import importlib.util
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent / "golden"
+    spec = importlib.util.spec_from_file_location("make_adversarial", here / "make_adversarial.py")
+    M = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(M)
+    with np.load(here / "adversarial_fma.npz") as z:
+        v, codes, scales = z["v_in"], z["v_codes"], z["v_scales"]
+    assert v.shape[2] >= 8
+    c, s = O.quantize_v(v)
+    assert np.array_equal(c, codes) and np.array_equal(s.view(np.uint32), scales.view(np.uint32))
+    for i in range(v.shape[2]):
+        rot = O.rotate(v[0, 0, i].astype(np.float64))
+        assert M.f32_scale(M.sumsq_numpy_order(rot)) == scales[0, 0, i]
+        assert M.f32_scale(M.sumsq_contracted(rot)) != scales[0, 0, i]

@@ -48,6 +48,8 @@ def fake_encode(ks, vs, g, codebook, sign_seed, k_scale_mode, device=None, check
         vv = v.values.reshape(-1).float()
         a.v_packed[i, :3 * n // 8] = (vv[: 3 * n // 8] * 1000).abs().round().remainder(256).to(torch.uint8)
         a.v_scales[i, :vecs] = v.values.reshape(vecs, -1).float().pow(2).mean(-1).sqrt()
+        if not bool(torch.isfinite(kv).all()):
+            a.status[i] |= 1  # PKV_FLAG_K_NONFINITE, as the device encoder reports it
     return None, None, a
 
 
@@ -83,6 +85,15 @@ def _worker(rank, world, port, q):
         qs = torch.arange(2 * 3 * 2 * 4, dtype=torch.float32).view(2, 3, 2, 4)
         out = parallel.decode_attention_head_sharded(lambda ql: ql * 2, qs, kv_heads=3)
         ok = ok and torch.equal(out, qs * 2)
+        # a data fault in a layer only rank 1 encodes: EVERY rank raises the
+        # reference's GeometryError after the collective (none hangs in it)
+        bad = _dump(g)
+        bad.layers[4][0].values[0, 1, 2, 3] = float("nan")
+        try:
+            parallel.build_pool_sharded(bad, encode_fn=fake_encode)
+            ok = False
+        except pk.GeometryError as exc:
+            ok = ok and "NaN or Inf" in str(exc) and "layer 4" in str(exc)
         q_ok = ok
     except Exception as exc:  # noqa: BLE001
         q_ok = repr(exc)
