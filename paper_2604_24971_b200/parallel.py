@@ -27,7 +27,6 @@ from .model import KvDump, ModelGeometry
 from .pool import SharedPool, _Arena, _encode_layers, pool_from_arena, raise_for_status
 from .valuequant import GAUSSIAN_3BIT, Codebook
 
-ARENA_FIELDS = ("k_codes", "k_scale", "k_bscale", "v_packed", "v_scales", "status")
 
 
 def _world(group) -> tuple[int, int]:
@@ -70,19 +69,21 @@ def _all_gather_rows(local: torch.Tensor, rows_max: int, group) -> torch.Tensor:
 
 
 def gather_arena(local: _Arena, num_layers: int, group=None) -> _Arena:
-    """Assemble the full [L, ...] arena from every rank's layer slice."""
+    """Assemble the full [L, layer_bytes] pool from every rank's layer slice
+    with ONE all-gather of the layer-major arena (pool._Arena): rank r's rows
+    are its layers' codes, packed values, scales and status words, already
+    back to back, so the collective moves exactly the packed pool bytes."""
     world, _ = _world(group)
+    local.status_row.copy_(local.status)  # status words travel inside the rows
     rows_max = len(layer_shard(num_layers, world, 0))
-    full = object.__new__(_Arena)
-    for name in ARENA_FIELDS:
-        t = getattr(local, name, None)
-        if t is None:
-            setattr(full, name, None)
-            continue
-        g = _all_gather_rows(t, rows_max, group)
-        pieces = [g[r, :len(layer_shard(num_layers, world, r))] for r in range(world)]
-        setattr(full, name, torch.cat(pieces, dim=0).contiguous())
-    full.replay = local.replay
+    g = _all_gather_rows(local.flat, rows_max, group)  # [world, rows_max, layer_bytes]
+    sizes = [len(layer_shard(num_layers, world, r)) for r in range(world)]
+    if all(sz == rows_max for sz in sizes):
+        flat = g.view(world * rows_max, local.layer_bytes)  # no compaction needed
+    else:
+        flat = torch.cat([g[r, :sizes[r]] for r in range(world)], dim=0).contiguous()
+    full = _Arena.like(local, flat)
+    full.replay = local.replay  # this rank's fp64-replay count
     return full
 
 
@@ -151,6 +152,6 @@ def decode_attention_head_sharded(attend: Callable[[torch.Tensor], torch.Tensor]
 
 
 __all__ = [
-    "ARENA_FIELDS", "all_reduce_layer_max", "build_pool_sharded", "decode_attention_head_sharded",
+    "all_reduce_layer_max", "build_pool_sharded", "decode_attention_head_sharded",
     "gather_arena", "head_shard", "layer_shard", "partition_agents",
 ]

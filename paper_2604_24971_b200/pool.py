@@ -117,19 +117,76 @@ class InjectionTranscript:
 # ---------------------------------------------------------------------------
 
 class _Arena:
-    """Device storage for L layers of one pool (see module docstring)."""
+    """Device storage for L layers of one pool, layer-major.
+
+    ONE uint8 allocation `flat` [L, layer_bytes]; each layer row holds that
+    layer's fields back to back, every section 256-byte aligned (TMA needs 16):
+        k_codes int8 [pad16(n)] | v_packed u8 [pad16(3 ceil(n/8))] |
+        v_scales f32 [pad4(vecs)] | k_bscale f16 [pad8(n/32)] (block32) |
+        k_scale f32 (tensor) | status i32 (gather copy)
+    The per-field attributes are strided [L, ...] views into `flat` (kernels
+    take per-layer pointers, so the row stride is invisible to them). A
+    layer-sharded pool is therefore ONE contiguous block per rank and the
+    multi-GPU assembly is ONE all_gather_into_tensor (parallel.gather_arena).
+    `status` (the per-launch contiguous status words the encoder ORs into)
+    and `replay` are small separate tensors.
+    """
+
+    ALIGN = 256
 
     def __init__(self, g: ModelGeometry, L: int, k_mode: str, device, with_k=True, with_v=True):
         n, vecs = g.elements_per_tensor, g.vectors_per_tensor
-        self.k_codes = torch.empty((L, _pad(n, 16)), dtype=torch.int8, device=device) if with_k else None
-        self.k_scale = torch.zeros(L, dtype=torch.float32, device=device) if (with_k and k_mode == "tensor") else None
-        self.k_bscale = (torch.empty((L, _pad(block32_count(n), 8)), dtype=torch.float16, device=device)
-                         if (with_k and k_mode == "block32") else None)
-        self.v_packed = torch.empty((L, _pad(packed_nbytes(n), 16)), dtype=torch.uint8, device=device) if with_v else None
-        # rows padded to 4 floats so every layer's scales start 16-byte aligned (TMA)
-        self.v_scales = torch.empty((L, _pad(vecs, 4)), dtype=torch.float32, device=device) if with_v else None
+        secs = []
+        if with_k:
+            secs.append(("k_codes", _pad(n, 16), torch.int8))
+        if with_v:
+            secs.append(("v_packed", _pad(packed_nbytes(n), 16), torch.uint8))
+            # rows padded to 4 floats so every layer's scales start 16-byte aligned (TMA)
+            secs.append(("v_scales", 4 * _pad(vecs, 4), torch.float32))
+        if with_k and k_mode == "block32":
+            secs.append(("k_bscale", 2 * _pad(block32_count(n), 8), torch.float16))
+        if with_k and k_mode == "tensor":
+            secs.append(("k_scale", 16, torch.float32))
+        secs.append(("status_row", 16, torch.int32))
+        offs, off = {}, 0
+        for name, nbytes, _ in secs:
+            offs[name] = off
+            off = _pad(off + nbytes, self.ALIGN)
+        self.layer_bytes = off
+        self.num_layers = L
+        self.k_mode = k_mode
+        self.flat = torch.empty((L, off), dtype=torch.uint8, device=device)
+        self._sections = [(name, offs[name], nbytes, dt) for name, nbytes, dt in secs]
+        self._bind()
+        if self.k_scale is not None:
+            self.k_scale.zero_()
         self.status = torch.zeros(L, dtype=torch.int32, device=device)
         self.replay = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def _bind(self):
+        for name in ("k_codes", "v_packed", "v_scales", "k_bscale", "k_scale", "status_row"):
+            setattr(self, name, None)
+        for name, off, nbytes, dt in self._sections:
+            v = self.flat[:, off:off + nbytes].view(dt)
+            if name in ("k_scale", "status_row"):
+                v = v[:, 0]
+            setattr(self, name, v)
+
+    @classmethod
+    def like(cls, other: "_Arena", flat: torch.Tensor) -> "_Arena":
+        """An arena with `other`'s layout around a given [L', layer_bytes] buffer
+        (e.g. the all-gathered pool)."""
+        a = object.__new__(cls)
+        a.layer_bytes, a.k_mode, a._sections = other.layer_bytes, other.k_mode, other._sections
+        a.num_layers = flat.shape[0]
+        a.flat = flat
+        a._bind()
+        a.status = a.status_row.contiguous()
+        a.replay = torch.zeros(1, dtype=torch.int32, device=flat.device)
+        return a
+
+    def nbytes(self) -> int:
+        return self.flat.numel() + 4 * self.status.numel()
 
 
 def _device_inputs(tensors, device):
@@ -386,6 +443,8 @@ class SharedPool:
 
     def device_nbytes(self) -> int:
         """Bytes the pool actually occupies in HBM (packed codes, scales, padding)."""
+        if self._arena is not None:
+            return self._arena.nbytes()
         tensors = self.k_codes + self.v_packed + self.v_scales + (self.k_scale or []) + (self.k_bscale or [])
         return sum(t.numel() * t.element_size() for t in tensors)
 
