@@ -271,57 +271,61 @@ def run_reference(args, cfg):
 # our implementation
 # ---------------------------------------------------------------------------
 def run_ours(args, cfg):
+    """Our arm. At N GPUs (one process per GPU, torchrun) the step is the
+    north_star pipeline with the config split over the GPUs: each rank
+    compresses its contiguous layer shard (one pkv_encode launch), ONE NCCL
+    all_gather_into_tensor replicates the packed pool (layer-major arena, so
+    the collective moves exactly the pool bytes), and each rank materialises
+    its shard to bf16 (one pkv_decode launch). Total work is fixed (strong
+    scaling); at N=1 the gather is absent. Decode attention: the config's
+    agents are partitioned over the ranks, each attending over its replica of
+    the whole pool (no per-step collective)."""
     import torch
     import torch.distributed as dist
 
     import paper_2604_24971_b200 as pk
-    from paper_2604_24971_b200 import _codec
+    from paper_2604_24971_b200 import _codec, parallel
     from paper_2604_24971_b200.attention import decode_attention
-    from paper_2604_24971_b200.pool import _Arena, _encode_layers, raise_for_status
+    from paper_2604_24971_b200.pool import _Arena, _encode_layers, pool_from_arena, raise_for_status
 
     L, H, D, T, agents, group, desc = cfg
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log (nRanks)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
-    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    in_b = 2 if dtype == torch.bfloat16 else 4
     g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
-    dump = pk.synth_gaussian_dump(g, seed=rank, device=dev, dtype=dtype, generator="torch")
-    ks = [k for k, _ in dump.layers]
-    vs = [v for _, v in dump.layers]
-    arena = _Arena(g, L, args.k_mode, dev)
-    kb, vb, _ = _encode_layers(ks, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena)
-    pool = pk.SharedPool(g, list(zip(kb, vb))).seal()
-    out_k = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in range(L)]
-    out_v = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    mine = list(parallel.layer_shard(L, world, rank))
+    my_agents = parallel.partition_agents(agents, world, rank)
+    rows_max = len(parallel.layer_shard(L, world, 0))
+    even = all(len(parallel.layer_shard(L, world, r)) == rows_max for r in range(world))
     stream = torch.cuda.current_stream(dev)
-
-    def encode():
-        _encode_layers(ks, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
-
-    def decode():
-        _codec.decode(num_vectors=g.vectors_per_tensor, head_dim=D, out_dtype=torch.bfloat16,
-                      k_mode=pk.keyquant.K_MODES[args.k_mode], k_codes=pool.k_codes, k_scale=pool.k_scale,
-                      k_bscale=pool.k_bscale, v_packed=pool.v_packed, v_scales=pool.v_scales,
-                      centroids=pk.GAUSSIAN_3BIT.centroids, sign_seed=None, k_out=out_k, v_out=out_v,
-                      device=dev)
-
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    none = [None] * L
+    n, vecs = g.elements_per_tensor, g.vectors_per_tensor
+    cb = pk.GAUSSIAN_3BIT
 
-    def encode_k():
-        _encode_layers(ks, none, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    def encode_v():
-        _encode_layers(none, vs, g, pk.GAUSSIAN_3BIT, None, args.k_mode, device=dev, arena=arena, check=False)
+    def barrier():
+        if world > 1:
+            dist.barrier()
 
     def capture(fn):
-        """CUDA-graph a launch sequence so the timed loop measures the GPU, not
-        the Python/ctypes enqueue path; None if capture is unavailable."""
+        """CUDA-graph a launch sequence (the timed loop then measures the GPU,
+        not the Python/ctypes enqueue path); None if capture is unavailable."""
         if args.no_graph:
             return None
         try:
@@ -336,143 +340,221 @@ def run_ours(args, cfg):
             torch.cuda.synchronize(dev)
             return gr.replay
         except Exception as exc:  # noqa: BLE001
-            print(f"[bench] graph capture unavailable ({exc}); timing eager launches", file=sys.stderr)
+            print(f"[bench] graph capture unavailable ({exc}); eager launches", file=sys.stderr)
             return None
 
-    for _ in range(args.warmup):
-        encode()
-        decode()
-    raise_for_status(arena.status)
-    torch.cuda.synchronize(dev)
-    run_enc = capture(encode) or encode
-    run_dec = capture(decode) or decode
-    run_enc_k = capture(encode_k) or encode_k
-    run_enc_v = capture(encode_v) or encode_v
-    graphed = not args.no_graph and run_enc is not encode
-    for _ in range(args.warmup):
-        run_enc()
-        run_dec()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    marks = [(ev(), ev(), ev()) for _ in range(args.steps)]
-    start, end = ev(), ev()
-    with ClockSampler(local) as clocks:
+    def shard_inputs(dtype):
+        """This rank's layers of a synthetic dump, drawn on the device."""
+        gen = torch.Generator(device=dev)
+        out = []
+        for li in mine:
+            gen.manual_seed(1000 + li)
+            k = torch.randn(g.tensor_shape, generator=gen, device=dev, dtype=torch.float32) * D ** -0.5
+            v = torch.randn(g.tensor_shape, generator=gen, device=dev, dtype=torch.float32) * D ** -0.5
+            out.append((pk.KvTensor(g, k.to(dtype)), pk.KvTensor(g, v.to(dtype))))
+        return out
+
+    def measure(dtype, steps, with_clocks=False):
+        """Time `steps` steps of encode(shard) [+ all-gather] + decode(shard)."""
+        in_b = 2 if dtype == torch.bfloat16 else 4
+        layers = shard_inputs(dtype)
+        ks = [k for k, _ in layers]
+        vs = [v for _, v in layers]
+        arena = _Arena(g, len(mine), args.k_mode, dev)
+        full_flat = (torch.empty((world * rows_max, arena.layer_bytes), dtype=torch.uint8, device=dev)
+                     if world > 1 else None)
+        out_k = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in mine]
+        out_v = [torch.empty(g.tensor_shape, dtype=torch.bfloat16, device=dev) for _ in mine]
+        kmode = pk.keyquant.K_MODES[args.k_mode]
+
+        def encode():
+            _encode_layers(ks, vs, g, cb, None, args.k_mode, device=dev, arena=arena, check=False)
+
+        def gather():
+            if world > 1:
+                arena.status_row.copy_(arena.status)
+                if even:
+                    dist.all_gather_into_tensor(full_flat, arena.flat)
+                else:
+                    parallel.gather_arena(arena, L)
+
+        def decode():
+            _codec.decode(num_vectors=vecs, head_dim=D, out_dtype=torch.bfloat16, k_mode=kmode,
+                          k_codes=[arena.k_codes[i] for i in range(len(mine))],
+                          k_scale=[arena.k_scale[i:i + 1] for i in range(len(mine))] if args.k_mode == "tensor" else None,
+                          k_bscale=[arena.k_bscale[i] for i in range(len(mine))] if args.k_mode == "block32" else None,
+                          v_packed=[arena.v_packed[i] for i in range(len(mine))],
+                          v_scales=[arena.v_scales[i, :vecs] for i in range(len(mine))],
+                          centroids=cb.centroids, sign_seed=None, k_out=out_k, v_out=out_v, device=dev)
+
+        for _ in range(args.warmup):
+            encode()
+            gather()
+            decode()
+        raise_for_status(arena.status)
+        torch.cuda.synchronize(dev)
+        run_enc, run_gat, run_dec = capture(encode) or encode, (capture(gather) if even else None) or gather, \
+            capture(decode) or decode
+        graphed = not args.no_graph and run_enc is not encode
+        for _ in range(args.warmup):
+            run_enc()
+            run_gat()
+            run_dec()
+        torch.cuda.synchronize(dev)
+        barrier()
+        marks = [(ev(), ev(), ev(), ev()) for _ in range(steps)]
+        start, end = ev(), ev()
+        clocks = ClockSampler(local) if with_clocks else None
+        if clocks:
+            clocks.__enter__()
         torch.cuda.synchronize(dev)
         start.record(stream)
-        for a_, b_, c_ in marks:
+        for a_, b_, c_, d_ in marks:
             a_.record(stream)
             run_enc()
             b_.record(stream)
-            run_dec()
+            run_gat()
             c_.record(stream)
+            run_dec()
+            d_.record(stream)
         end.record(stream)
         torch.cuda.synchronize(dev)
-    total_ms = start.elapsed_time(end)
-    enc_ms = sum(a_.elapsed_time(b_) for a_, b_, _ in marks) / args.steps
-    dec_ms = sum(b_.elapsed_time(c_) for _, b_, c_ in marks) / args.steps
-
-    def time_it(fn, n):
-        s_, e_ = ev(), ev()
-        fn()
-        torch.cuda.synchronize(dev)
-        s_.record(stream)
-        for _ in range(n):
-            fn()
-        e_.record(stream)
-        torch.cuda.synchronize(dev)
-        return s_.elapsed_time(e_) / n
-
-    enc_k_ms = time_it(run_enc_k, args.steps)
-    enc_v_ms = time_it(run_enc_v, args.steps)
-    def max_over_ranks(ms):
+        if clocks:
+            clocks.__exit__(None, None, None)
+        res = {
+            "ms_step": max_over_ranks(start.elapsed_time(end) / steps),
+            "encode_ms": sum(a_.elapsed_time(b_) for a_, b_, _, _ in marks) / steps,
+            "gather_ms": sum(b_.elapsed_time(c_) for _, b_, c_, _ in marks) / steps,
+            "decode_ms": sum(c_.elapsed_time(d_) for _, _, c_, d_ in marks) / steps,
+            "graphed": graphed, "in_b": in_b, "clocks": clocks.summary() if clocks else None,
+            "replays": int(arena.replay.item()), "arena": arena, "full_flat": full_flat,
+        }
+        comp_b, deq_b = algorithmic_bytes(L, H, D, T, in_b, 2, args.k_mode)
+        res["comp_b"], res["deq_b"] = comp_b, deq_b
+        res["value"] = (comp_b + deq_b) / (res["ms_step"] / 1e3) / 1e9
         if world == 1:
-            return ms
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+            none = [None] * len(mine)
 
-    total_ms = max_over_ranks(total_ms)
-    ms_step = total_ms / args.steps
-    comp_b, deq_b = algorithmic_bytes(L, H, D, T, in_b, 2, args.k_mode)
-    value = world * (comp_b + deq_b) / (ms_step / 1e3) / 1e9
+            def time_it(fn, k):
+                s_, e_ = ev(), ev()
+                fn()
+                torch.cuda.synchronize(dev)
+                s_.record(stream)
+                for _ in range(k):
+                    fn()
+                e_.record(stream)
+                torch.cuda.synchronize(dev)
+                return s_.elapsed_time(e_) / k
+
+            enc_k = capture(lambda: _encode_layers(ks, none, g, cb, None, args.k_mode, device=dev, arena=arena,
+                                                   check=False))
+            enc_v = capture(lambda: _encode_layers(none, vs, g, cb, None, args.k_mode, device=dev, arena=arena,
+                                                   check=False))
+            if enc_k and enc_v:
+                res["encode_keys_ms"] = time_it(enc_k, steps)
+                res["encode_values_ms"] = time_it(enc_v, steps)
+        return res
+
+    main_dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    other_dt = torch.float32 if main_dt == torch.bfloat16 else torch.bfloat16
+    r = measure(main_dt, args.steps, with_clocks=True)
+    variant = None if args.skip_variant else measure(other_dt, max(5, min(args.steps, 50)))
+    ms_step, value, comp_b, deq_b, in_b = r["ms_step"], r["value"], r["comp_b"], r["deq_b"], r["in_b"]
+
+    # the pool every rank now holds (gathered), for attention
+    arena = r["arena"]
+    if world > 1:
+        full = _Arena.like(arena, r["full_flat"][:L]) if even else parallel.gather_arena(arena, L)
+        raise_for_status(full.status)  # every rank's status words travelled inside the rows
+        pool = pool_from_arena(full, g, cb, None, args.k_mode)
+    else:
+        pool = pool_from_arena(arena, g, cb, None, args.k_mode)
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.skip_e2e:
-        host_layers = [(k.values.cpu().pin_memory(), v.values.cpu().pin_memory()) for k, v in dump.layers]
-        host_dump = pk.KvDump(g, tuple((pk.KvTensor(g, k), pk.KvTensor(g, v)) for k, v in host_layers))
+        host = [(k.values.cpu().pin_memory(), v.values.cpu().pin_memory()) for k, v in shard_inputs(main_dt)]
+        placeholder = host[0]
+        by_layer = dict(zip(mine, host))
+        host_dump = pk.KvDump(g, tuple((pk.KvTensor(g, by_layer.get(i, placeholder)[0]),
+                                        pk.KvTensor(g, by_layer.get(i, placeholder)[1])) for i in range(L)))
         host_out = [(torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory(),
-                     torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in range(L)]
-
+                     torch.empty(g.tensor_shape, dtype=torch.bfloat16).pin_memory()) for _ in mine]
         inflight = []
 
         def e2e_step():
-            # build_pool uploads the pinned dump chunk by chunk, overlapped with
-            # the encode; materialize_to_host overlaps decode with the D2H copies.
-            # The host may run one step ahead (step n+1 uploads while step n
-            # downloads) but no further: unbounded run-ahead makes the caching
-            # allocator grow (cudaMalloc stalls the host for 100s of ms).
-            p = pk.build_pool(host_dump, build_stats=False, device=dev, check=False)
-            p.attach(16).materialize_to_host(host_out)
+            # build uploads the pinned inputs (chunk-wise, overlapped with the
+            # encode), materialize_to_host overlaps decode with the D2H copies.
+            # The host may run one step ahead but no further (unbounded
+            # run-ahead grows the caching allocator: cudaMalloc stalls).
+            if world == 1:
+                p = pk.build_pool(host_dump, build_stats=False, device=dev, check=False)
+            else:
+                p = parallel.build_pool_sharded(host_dump, device=dev, check=False)
+            p.attach(16).materialize_to_host(host_out, layers=mine)
             done = torch.cuda.Event()
             done.record(stream)
             inflight.append(done)
             if len(inflight) > 1:
                 inflight.pop(0).synchronize()
 
-        # warm the caching allocator (each step allocates a fresh pool and
-        # staging buffers; the first steps pay cudaMalloc) before timing
         for _ in range(max(3, args.warmup)):
             e2e_step()
         torch.cuda.synchronize(dev)
         es, ee = ev(), ev()
         n_e2e = max(3, min(args.steps, 20))
-        if world > 1:
-            dist.barrier()
+        barrier()
         es.record(stream)
         for _ in range(n_e2e):
             e2e_step()
         ee.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = max_over_ranks(es.elapsed_time(ee) / n_e2e)
-        h2d = 2 * L * g.elements_per_tensor * in_b
-        d2h = 2 * L * g.elements_per_tensor * 2
-        e2e = {"value": world * (comp_b + deq_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+        e2e = {"value": (comp_b + deq_b) / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 2 * L * n * in_b, "d2h_bytes_per_step": 2 * L * n * 2,
+               "ms_per_step": e2e_ms, "api": "build_pool / parallel.build_pool_sharded + "
+                                             "attach(16).materialize_to_host (pinned host in and out)",
+               "bytes_note": "h2d/d2h summed over all ranks (each rank moves its layer shard)"}
 
-    # ---- shared-pool decode attention (all agents, all layers) ----
+    # ---- shared-pool decode attention: agents partitioned over ranks ----
     attn = None
     if not args.skip_attention and D in (64, 128):
-        q = torch.randn(agents, H, group, D, device=dev, dtype=torch.bfloat16)
-        outa = torch.empty_like(q)
-        need = pk._lib.load().pkv_attention_workspace_bytes(agents, H, group, D, T)
-        ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=dev)
+        a_ms = 0.0
+        if my_agents:
+            q = torch.randn(len(my_agents), H, group, D, device=dev, dtype=torch.bfloat16)
+            outa = torch.empty_like(q)
+            need = pk._lib.load().pkv_attention_workspace_bytes(len(my_agents), H, group, D, T)
+            ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=dev)
 
-        def attn_step():
-            for li in range(L):
-                decode_attention(pool, li, q, softmax_scale=D ** -0.5, out=outa, workspace=ws)
+            def attn_step():
+                for li in range(L):
+                    decode_attention(pool, li, q, softmax_scale=D ** -0.5, out=outa, workspace=ws)
 
-        for _ in range(2):
-            attn_step()
-        torch.cuda.synchronize(dev)
-        s2, e2 = ev(), ev()
-        if world > 1:
-            dist.barrier()
-        s2.record(stream)
-        for _ in range(args.steps):
-            attn_step()
-        e2.record(stream)
-        torch.cuda.synchronize(dev)
-        a_ms = max_over_ranks(s2.elapsed_time(e2) / args.steps)
-        pool_bytes = L * (g.elements_per_tensor * (1 + 3 / 8) + 4 * g.vectors_per_tensor + 4)
-        attn = {"tokens_per_s": world * agents / (a_ms / 1e3), "ms_per_token_step": a_ms,
-                "agents": agents, "layers": L, "scope": "attention only (all layers), batched agents",
-                "pool_gbs": pool_bytes / (a_ms / 1e3) / 1e9}
+            run_attn = capture(attn_step) or attn_step
+            for _ in range(3):
+                run_attn()
+            torch.cuda.synchronize(dev)
+        barrier()
+        if my_agents:
+            s2, e2 = ev(), ev()
+            s2.record(stream)
+            for _ in range(args.steps):
+                run_attn()
+            e2.record(stream)
+            torch.cuda.synchronize(dev)
+            a_ms = s2.elapsed_time(e2) / args.steps
+        a_ms = max_over_ranks(a_ms)
+        pool_bytes = L * (n * (1 + 3 / 8) + 4 * vecs + 4)
+        flops = 4.0 * L * agents * group * T * D  # q.k and p.v per query row, all layers
+        attn = {"tokens_per_s": agents / (a_ms / 1e3), "ms_per_token_step": a_ms, "agents": agents,
+                "agents_per_rank": len(my_agents), "layers": L,
+                "scope": "attention only (all layers), each rank batches its agents over its pool replica",
+                "pool_gbs_per_rank": pool_bytes / (a_ms / 1e3) / 1e9,
+                "tflops": flops / (a_ms / 1e3) / 1e12 if world == 1 else None}
 
     # ---- model-level shared-pool decode (random-init model of the config's shape) ----
     dec_e2e = None
-    if not args.skip_decode_e2e and args.config in ("c2", "c3") and rank == 0:
+    if not args.skip_decode_e2e and args.config in ("c2", "c3") and rank == 0 and world == 1:
         try:
             sys.path.insert(0, str(ROOT / "tools"))
             import decode_bench
@@ -485,23 +567,36 @@ def run_ours(args, cfg):
             dec_e2e = {"error": repr(exc)[:300]}
 
     peak, peak_kind = measured_peaks()
-    n = g.elements_per_tensor
-    vecs = g.vectors_per_tensor
-    kb = 4 if args.k_mode == "tensor" else 2 * ((n + 31) // 32)
-    bytes_k = L * (n * in_b + n + kb)                      # key encode (absmax pass + codes)
-    bytes_v = L * (n * in_b + 3 * n / 8 + 4 * vecs)        # value encode
-    # the step's two launches: the fused encode (value + key roles) and the decode
-    kernels = {"encode": (enc_ms, comp_b), "decode": (dec_ms, deq_b)}
+    kscale_b = 4 if args.k_mode == "tensor" else 2 * ((n + 31) // 32)
+    Lr = len(mine)
+    enc_bytes = Lr * (2 * n * in_b + n + kscale_b + 3 * n / 8 + 4 * vecs)   # this rank's shard
+    dec_bytes = Lr * (n + kscale_b + 3 * n / 8 + 4 * vecs + 2 * n * 2)
+    kernels = {"encode": (r["encode_ms"], enc_bytes), "decode": (r["decode_ms"], dec_bytes)}
     dom_name = max(kernels, key=lambda k: kernels[k][0])
     dom_ms, dom_bytes = kernels[dom_name]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    prof = ROOT / "profiles" / "traffic.json"
     traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get(f"{args.config}/{args.dtype}/{dom_name}")
         except Exception:
             traffic = None
+
+    def kernel_block(res, label):
+        d = {"dtype_in": label, "step_ms": res["ms_step"], "value_gbs": res["value"],
+             "encode_ms": res["encode_ms"], "decode_ms": res["decode_ms"],
+             "encode_gbs_per_gpu": Lr * (2 * n * res["in_b"] + n + kscale_b + 3 * n / 8 + 4 * vecs)
+             / (res["encode_ms"] / 1e3) / 1e9,
+             "decode_gbs_per_gpu": dec_bytes / (res["decode_ms"] / 1e3) / 1e9,
+             "cuda_graph": res["graphed"], "replayed_vectors": res["replays"]}
+        if world > 1:
+            d["gather_ms"] = res["gather_ms"]
+        if "encode_keys_ms" in res:
+            d["encode_keys_ms"] = res["encode_keys_ms"]
+            d["encode_values_ms"] = res["encode_values_ms"]
+        d["encode_frac_of_peak"] = d["encode_gbs_per_gpu"] / peak
+        return d
 
     cpu = None
     if rank == 0 and not args.skip_cpu:
@@ -512,44 +607,86 @@ def run_ours(args, cfg):
             sec = ref.step(L)
         finally:
             ref.close()
-        cb, dbb = algorithmic_bytes(L, H, D, T, 4, 2)
-        cpu = {"value": (cb + dbb) / sec / 1e9, "unit": "GB/s", "cores": ref.procs, "kind": ref.kind,
+        cbb, dbb = algorithmic_bytes(L, H, D, T, 4, 2)
+        cpu = {"value": (cbb + dbb) / sec / 1e9, "unit": "GB/s", "cores": ref.procs, "kind": ref.kind,
                "sample": f"all {L} layers [1,{H},{T},{D}] f32, one step: stock kvpool build_pool + "
                          f"attach(16).get_kv_for_layer per layer, {ref.procs} processes",
                **cpu_info()}
 
     if rank == 0:
+        dtn = "f32" if main_dt == torch.float32 else "bf16"
+        par = ("1 GPU: the whole pool" if world == 1 else
+               f"layer-sharded build ({rows_max} layers/GPU) + one NCCL all-gather of the packed pool "
+               f"(replicated on every GPU) + materialise of each GPU's layers; decode agents partitioned "
+               f"{[len(parallel.partition_agents(agents, world, x)) for x in range(world)]}")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16 in / u8+int8 pool / bf16 out" if in_b == 2 else "f32 in / u8+int8 pool / bf16 out",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": f"{dtn} in / u8+int8 pool / bf16 out",
             "data": "synthetic (torch.randn, var 1/head_dim, random-init)",
             "config": {"workload": desc, "layers": L, "kv_heads": H, "head_dim": D, "seq_len": T,
-                       "agents": agents, "k_scale_mode": args.k_mode,
-                       "step": "build_pool (pkv_encode, all layers) + inject_all to bf16 (pkv_decode, all layers)",
-                       "l2": "inputs larger than L2 (no flush needed)",
-                       "parallelism": f"replica x{world} (independent pools per GPU)"},
+                       "agents": agents, "k_scale_mode": args.k_mode, "input_dtype": dtn,
+                       "step": "build_pool (pkv_encode) + inject to bf16 (pkv_decode) of every layer; "
+                               "at N>1 + the pool all-gather",
+                       "l2": "inputs larger than L2 (no flush needed)", "parallelism": par},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
-                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic},
-            "kernels": {"encode_ms": enc_ms, "encode_gbs": comp_b / (enc_ms / 1e3) / 1e9,
-                        "decode_ms": dec_ms, "decode_gbs": deq_b / (dec_ms / 1e3) / 1e9,
-                        "encode_values_ms": enc_v_ms, "encode_values_gbs": bytes_v / (enc_v_ms / 1e3) / 1e9,
-                        "encode_keys_ms": enc_k_ms, "encode_keys_gbs": bytes_k / (enc_k_ms / 1e3) / 1e9,
-                        "encode_bytes": comp_b, "decode_bytes": deq_b, "cuda_graph": graphed},
-            # per step: one encode launch (value + key roles) and one decode launch (+ one memset)
-            "gpu_launches": 2 * args.steps,
-            "clocks": clocks.summary(),
+                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic},
+            "kernels": kernel_block(r, dtn),
+            "variant": kernel_block(variant, "bf16" if dtn == "f32" else "f32") if variant else None,
+            # per step: encode + decode (+ the all-gather at N>1; + one workspace memset)
+            "gpu_launches": (2 + (1 if world > 1 else 0)) * args.steps,
+            "clocks": r["clocks"],
             "e2e": e2e,
             "decode_attention": attn,
             "decode_e2e": dec_e2e,
-            "replayed_vectors_per_build": pool.replay_count,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def print_plan(args, cfg) -> int:
+    """The sharding plan every rank computes, gathered to rank 0 over gloo
+    (exercises the self-launch, rendezvous and partitioning without a GPU)."""
+    import torch.distributed as dist
+
+    from paper_2604_24971_b200 import parallel
+
+    L, H, D, T, agents, group, desc = cfg
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    mine = {"rank": rank, "layers": list(parallel.layer_shard(L, world, rank)),
+            "agents": parallel.partition_agents(agents, world, rank)}
+    plans = [mine]
+    if world > 1:
+        dist.init_process_group("gloo")
+        plans = [None] * world
+        dist.all_gather_object(plans, mine)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"config": args.config, "world": world, "plan": plans}), flush=True)
+    return 0
+
+
+def launch_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-run this script as N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1, NCCL_DEBUG=INFO."""
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -559,17 +696,26 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--dtype", default="f32", choices=["bf16", "f32"],
+                    help="input dtype of the headline (f32: the reference's dtype, SURVEY 8(d)); "
+                         "the other one is measured as the variant")
     ap.add_argument("--k-mode", default="tensor", choices=["tensor", "block32"])
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-attention", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graphs")
     ap.add_argument("--skip-decode-e2e", action="store_true", help="skip the model-level decode measurement")
+    ap.add_argument("--skip-variant", action="store_true", help="skip the other input dtype's measurement")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print each rank's layer / agent shard (gloo; no GPU work) and exit")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    if args.plan_only:
+        return print_plan(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

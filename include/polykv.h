@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PKV_ABI_VERSION 2
+#define PKV_ABI_VERSION 3
 
 /* status codes */
 #define PKV_OK 0
@@ -104,6 +104,13 @@ size_t pkv_encode_workspace_bytes(int num_layers, int64_t num_vectors, int head_
  *  status            device uint32[num_layers], OR-ed with PKV_FLAG_* bits.
  *  replay_count      device uint32[1] or NULL: incremented once per head vector
  *                    that was re-coded on the exact fp64 path.
+ *  k_layer_max       NULL (the per-tensor key scale comes from this call's
+ *                    own max|K| pass), or device uint32[num_layers]: the f32
+ *                    bit patterns of max|K| per layer computed elsewhere --
+ *                    e.g. MAX-reduced over the GPUs that each hold some of a
+ *                    layer's KV heads (pkv_k_absmax + an all-reduce); the
+ *                    scale is then f32(max/127) exactly as keyquant.py:55-60.
+ *                    Ignored for PKV_K_BLOCK32.
  *  workspace         device scratch of pkv_encode_workspace_bytes(num_layers,
  *                    num_vectors, head_dim).
  */
@@ -113,8 +120,17 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
                uint16_t* const* k_bscale, uint8_t* const* v_packed,
                float* const* v_scales, const double* centroids_host,
                const uint32_t* sign_bits_host, uint32_t* status,
-               uint32_t* replay_count, void* workspace,
-               size_t workspace_bytes, void* stream);
+               uint32_t* replay_count, const uint32_t* k_layer_max,
+               void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * pkv_k_absmax — max|K| of each of `num_layers` key tensors of `count`
+ * elements (f32 or bf16), as f32 bit patterns in device uint32 max_bits[l]
+ * (zeroed first; NaN inputs give a pattern above +inf). The per-rank half of
+ * keyquant.py:55 when a layer's heads are sharded over GPUs.
+ */
+int pkv_k_absmax(int num_layers, int64_t count, int in_dtype,
+                 const void* const* k_in, uint32_t* max_bits, void* stream);
 
 /*
  * pkv_decode — materialising read for `num_layers` layers in one launch.

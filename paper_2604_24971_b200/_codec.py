@@ -88,7 +88,10 @@ def encode(
     status: torch.Tensor,
     replay: torch.Tensor | None,
     device: torch.device,
+    k_layer_max: torch.Tensor | None = None,
 ) -> None:
+    """pkv_encode. k_layer_max: optional int32 [L] device tensor of external
+    per-layer max|K| bit patterns (head-sharded pools); None = own pass."""
     lib = load()
     ins = k_in if k_in is not None else v_in
     L = len(ins)
@@ -106,9 +109,21 @@ def encode(
         arr(k_in), arr(v_in), k_mode,
         arr(k_codes), arr(k_scale), arr(k_bscale), arr(v_packed), arr(v_scales),
         centroid_array(centroids), sign_word_array(sign_seed, head_dim),
-        status.data_ptr(), _p(replay), ws.data_ptr(), ws_bytes, stream_ptr(device),
+        status.data_ptr(), _p(replay), _p(k_layer_max), ws.data_ptr(), ws_bytes, stream_ptr(device),
     )
     check(rc, "pkv_encode")
+
+
+def k_absmax(k_in: list[torch.Tensor], out: torch.Tensor, device: torch.device) -> torch.Tensor:
+    """pkv_k_absmax: out[l] = f32 bit pattern of max|k_in[l]| (int32 [L] on device)."""
+    lib = load()
+    for t in k_in:
+        if t.device != device or not t.is_contiguous() or t.dtype != k_in[0].dtype:
+            raise ValueError("absmax inputs must be contiguous same-dtype tensors on the device")
+    rc = lib.pkv_k_absmax(len(k_in), k_in[0].numel(), dtype_code(k_in[0]), ptr_array([t.data_ptr() for t in k_in]),
+                          out.data_ptr(), stream_ptr(device))
+    check(rc, "pkv_k_absmax")
+    return out
 
 
 def decode(

@@ -46,8 +46,9 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_int, c_i64, c_int, c_int, P(c_void_p), P(c_void_p), c_int, P(c_void_p), P(c_void_p),
          P(c_void_p), P(c_void_p), P(c_void_p), P(ctypes.c_double), P(ctypes.c_uint32), c_void_p,
-         c_void_p, c_void_p, c_size, c_void_p],
+         c_void_p, c_void_p, c_void_p, c_size, c_void_p],
     ),
+    "pkv_k_absmax": (c_int, [c_int, c_i64, c_int, P(c_void_p), c_void_p, c_void_p]),
     "pkv_decode": (
         c_int,
         [c_int, c_i64, c_int, c_int, c_int, P(c_void_p), P(c_void_p), P(c_void_p), P(c_void_p),

@@ -965,7 +965,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
                int8_t* const* k_codes, float* const* k_scale, uint16_t* const* k_bscale,
                uint8_t* const* v_packed, float* const* v_scales, const double* centroids_host,
                const uint32_t* sign_bits_host, uint32_t* status, uint32_t* replay_count,
-               void* workspace, size_t workspace_bytes, void* stream) {
+               const uint32_t* k_layer_max, void* workspace, size_t workspace_bytes, void* stream) {
   if (num_layers < 0 || num_vectors < 0 || head_dim < 1) return PKV_ERR_INVALID_ARG;
   if (in_dtype != PKV_F32 && in_dtype != PKV_BF16) return PKV_ERR_INVALID_ARG;
   if (k_mode != PKV_K_TENSOR && k_mode != PKV_K_BLOCK32) return PKV_ERR_INVALID_ARG;
@@ -1039,6 +1039,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
       q.sign = sign;
       q.status = status + l0;
       q.replay_count = replay_count;
+      q.k_max_ext = (do_k && k_mode == PKV_K_TENSOR && k_layer_max) ? k_layer_max + l0 : nullptr;
       q.ws = workspace;
       q.ws_bytes = workspace_bytes;
       const int src = stream::encode(q, st);
@@ -1048,7 +1049,8 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     a.vec_ok = ok ? 1 : 0;
     const int k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;
     a.e_items = k_items;
-    a.a_items = (do_k && k_mode == PKV_K_TENSOR) ? k_items : 0;
+    const bool ext_max = do_k && k_mode == PKV_K_TENSOR && k_layer_max;
+    a.a_items = (do_k && k_mode == PKV_K_TENSOR && !ext_max) ? k_items : 0;
     a.v_items = do_v ? v_items_dispatch(head_dim, num_vectors) : 0;
     // lag: keep >= ~2 waves of warps between a layer's absmax and its key encode
     const long long round = (long long)a.a_items + a.v_items + a.e_items;
@@ -1068,6 +1070,11 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     a.round_start[a.num_rounds] = acc;
     a.total_items = acc;
     if (cudaMemsetAsync(workspace, 0, (size_t)(2 * L + 2) * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
+    // external per-layer maxima: the key encode reads them where the absmax
+    // items would have left theirs (and, with a_items == 0, never waits)
+    if (ext_max && cudaMemcpyAsync(workspace, k_layer_max + l0, (size_t)L * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return PKV_ERR_CUDA;
     const bool sym = do_v ? a.cb.symmetric != 0 : true;
     const int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st, do_v, sym, sign)
                                        : dispatch_encode<__nv_bfloat16>(a, st, do_v, sym, sign);

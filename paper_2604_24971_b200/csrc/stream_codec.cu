@@ -137,6 +137,7 @@ struct EncArgs {
   uint32_t* replay_count;
   unsigned int* layer_max;  // [L] max |K| bits (published by the key-role CTAs)
   unsigned int* layer_done;   // [L] absmax items folded into layer_max (per-tensor mode)
+  const uint32_t* k_max_ext;  // per-tensor keys: external max|K| bits per layer (no absmax pass)
   int value_ctas;             // CTAs [0, value_ctas) encode values, the rest keys
   int nA;                     // absmax items per layer (per-tensor mode)
   int nseg;                   // key-role segments of nE items: kind (A/E) + layer
@@ -1103,6 +1104,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     tma::fence_mbar_init();
   }
   if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
+  if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
   if (threadIdx.x < kMaxGroups * kMaxSG) {
     (&ctl->gmax[0][0])[threadIdx.x] = 0;
     (&ctl->gcnt[0][0])[threadIdx.x] = 0;
@@ -1587,7 +1589,8 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   // key encode) are HBM-bound, and the two overlap.
   const int dk = do_v ? r.head_dim : 64;  // key-only launches never touch the value tile geometry
   if (rc == PKV_OK) {
-    a->nA = (do_k && r.k_mode == PKV_K_TENSOR) ? a->nE : 0;
+    a->k_max_ext = r.k_max_ext;
+    a->nA = (do_k && r.k_mode == PKV_K_TENSOR && !r.k_max_ext) ? a->nE : 0;
     a->layer_done = w32 + L;
     const int grid = sm_count();  // one CTA per SM (checked by the launcher)
     // key-role segment order (see enc_key_item_at)

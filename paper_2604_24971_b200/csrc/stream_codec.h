@@ -26,6 +26,7 @@ struct EncodeRequest {
   bool sign;
   uint32_t* status;
   uint32_t* replay_count;
+  const uint32_t* k_max_ext;  // per-tensor keys: external max|K| bits per layer (null: own absmax pass)
   void* ws;  // workspace_bytes(num_layers, num_vectors, head_dim)
   size_t ws_bytes;
 };

@@ -23,8 +23,9 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-from .model import KvDump, ModelGeometry
-from .pool import SharedPool, _Arena, _encode_layers, pool_from_arena, raise_for_status
+from . import _codec
+from .model import KvDump, KvTensor, ModelGeometry
+from .pool import SharedPool, _Arena, _device_inputs, _encode_layers, pool_from_arena, raise_for_status
 from .valuequant import GAUSSIAN_3BIT, Codebook
 
 
@@ -89,7 +90,7 @@ def gather_arena(local: _Arena, num_layers: int, group=None) -> _Arena:
 
 def build_pool_sharded(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_seed: int | None = None, *,
                        k_scale_mode: str = "tensor", group=None, device=None,
-                       encode_fn: Callable | None = None) -> SharedPool:
+                       encode_fn: Callable | None = None, check: bool = True) -> SharedPool:
     """build_pool (pool.py:258-293) with the layers spread over the ranks of `group`.
 
     Each rank reads only its own layers of `dump`; the returned pool is the
@@ -114,7 +115,8 @@ def build_pool_sharded(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_se
     # GATHERED status words, so every rank sees every rank's faults and raises
     # the same exception after the collective; raising before it would leave
     # the healthy ranks blocked in all_gather.
-    raise_for_status(full.status)
+    if check:
+        raise_for_status(full.status)
     return pool_from_arena(full, g, codebook, sign_seed, k_scale_mode)
 
 
@@ -131,6 +133,83 @@ def all_reduce_layer_max(local_max_bits: torch.Tensor, group=None) -> torch.Tens
 
 def head_shard(kv_heads: int, world: int, rank: int) -> range:
     return layer_shard(kv_heads, world, rank)
+
+
+def head_geometry(g: ModelGeometry, heads: range) -> ModelGeometry:
+    return ModelGeometry(num_layers=g.num_layers, kv_heads=len(heads), head_dim=g.head_dim, seq_len=g.seq_len,
+                         batch=g.batch, baseline_bits=g.baseline_bits)
+
+
+def head_slice(t: KvTensor, heads: range, g_local: ModelGeometry) -> KvTensor:
+    """[B, H, T, D] -> [B, len(heads), T, D]: the KV heads this rank owns
+    (a view for batch 1, where a head range is contiguous)."""
+    v = t.values[:, heads.start:heads.stop]
+    return KvTensor(g_local, v if v.is_contiguous() else v.contiguous())
+
+
+def local_key_max(ks, device) -> torch.Tensor:
+    """int32 [L]: max|K| bit pattern of each layer's local key slice (pkv_k_absmax)."""
+    dev = _codec.require_device(device if device is not None else ks[0].values.device)
+    vals = _device_inputs(ks, dev)
+    out = torch.empty(len(vals), dtype=torch.int32, device=dev)
+    return _codec.k_absmax(vals, out, dev)
+
+
+def _or_status_over_ranks(status: torch.Tensor, group) -> torch.Tensor:
+    world, _ = _world(group)
+    if world == 1:
+        return status
+    parts = _all_gather_rows(status.view(1, -1), 1, group)  # [world, 1, L]
+    acc = parts[0, 0].clone()
+    for r in range(1, world):
+        acc |= parts[r, 0]
+    return acc
+
+
+def build_pool_head_sharded(dump: KvDump, codebook: Codebook = GAUSSIAN_3BIT, sign_seed: int | None = None, *,
+                            k_scale_mode: str = "tensor", group=None, device=None, heads: range | None = None,
+                            reduce_max: Callable | None = None, absmax_fn: Callable | None = None,
+                            encode_fn: Callable | None = None, check: bool = True) -> SharedPool:
+    """build_pool (pool.py:258-293) for the KV heads `heads` (default: this
+    rank's head_shard) of every layer -- the head-sharded alternative of
+    SURVEY §8(e): the pool stays split by KV head across the ranks.
+
+    The only cross-rank dependency of the codec is the per-tensor key scale,
+    f32(max|K| / 127) over the WHOLE layer (keyquant.py:55-60): each rank
+    takes the max of its heads (pkv_k_absmax), the ranks MAX-reduce the bit
+    patterns (all_reduce_layer_max; `reduce_max` overrides, e.g. a
+    precomputed global max), and pkv_encode uses the reduced maxima
+    (k_layer_max), so every rank's codes equal the single-GPU build's codes
+    for its heads, bit for bit. Block32 keys and values need no collective.
+    Data faults are OR-ed over the ranks before raising, so all ranks agree.
+    Returns a pool over the local heads (geometry kv_heads = len(heads));
+    `pool.head_range` / `pool.full_geometry` describe the slice.
+    """
+    g: ModelGeometry = dump.geometry
+    world, rank = _world(group)
+    hs = heads if heads is not None else head_shard(g.kv_heads, world, rank)
+    if len(hs) == 0:
+        raise ValueError(f"rank {rank} owns no KV heads ({g.kv_heads} heads over {world} ranks)")
+    if g.batch != 1 and (hs.start, hs.stop) != (0, g.kv_heads):
+        raise ValueError("head sharding needs batch 1 (a head range is then contiguous)")
+    gl = head_geometry(g, hs)
+    ks = [head_slice(k, hs, gl) for k, _ in dump.layers]
+    vs = [head_slice(v, hs, gl) for _, v in dump.layers]
+    if device is None and torch.cuda.is_available():
+        device = torch.device("cuda", torch.cuda.current_device())
+    kmax = None
+    if k_scale_mode == "tensor":
+        local = (absmax_fn or local_key_max)(ks, device)
+        kmax = reduce_max(local) if reduce_max is not None else all_reduce_layer_max(local, group)
+    _, _, arena = (encode_fn or _encode_layers)(ks, vs, gl, codebook, sign_seed, k_scale_mode, device=device,
+                                                check=False, k_layer_max=kmax)
+    status = _or_status_over_ranks(arena.status, group)
+    if check:
+        raise_for_status(status)
+    pool = pool_from_arena(arena, gl, codebook, sign_seed, k_scale_mode)
+    pool.head_range = hs
+    pool.full_geometry = g
+    return pool
 
 
 def decode_attention_head_sharded(attend: Callable[[torch.Tensor], torch.Tensor], q: torch.Tensor,
@@ -152,6 +231,7 @@ def decode_attention_head_sharded(attend: Callable[[torch.Tensor], torch.Tensor]
 
 
 __all__ = [
-    "all_reduce_layer_max", "build_pool_sharded", "decode_attention_head_sharded",
+    "all_reduce_layer_max", "build_pool_head_sharded", "build_pool_sharded", "decode_attention_head_sharded",
+    "head_geometry", "head_slice", "local_key_max",
     "gather_arena", "head_shard", "layer_shard", "partition_agents",
 ]

@@ -213,9 +213,12 @@ def raise_for_status(status: torch.Tensor) -> None:
 
 
 def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, sign_seed,
-                   k_scale_mode: str, *, device=None, check: bool = True, arena: _Arena | None = None):
+                   k_scale_mode: str, *, device=None, check: bool = True, arena: _Arena | None = None,
+                   k_layer_max: torch.Tensor | None = None):
     """Encode parallel lists of K / V KvTensors (entries may be None) with one
-    pkv_encode launch per input dtype. Returns (key blocks, value blocks, arena)."""
+    pkv_encode launch per input dtype. Returns (key blocks, value blocks, arena).
+    k_layer_max: optional int32 [L] device tensor of per-layer max|K| bit
+    patterns (head-sharded pools) replacing the encoder's own absmax pass."""
     if k_scale_mode not in K_MODES:
         raise ValueError(f"k_scale_mode must be one of {tuple(K_MODES)}, got {k_scale_mode!r}")
     ref = next(t for t in list(ks) + list(vs) if t is not None)
@@ -265,7 +268,9 @@ def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, s
                 v_packed=[a.v_packed[i] for i in vg] if vg else None,
                 v_scales=[a.v_scales[i, :g.vectors_per_tensor] for i in vg] if vg else None,
                 centroids=(codebook.centroids if codebook is not None else np.zeros(8)),
-                sign_seed=sign_seed, status=status, replay=a.replay, device=device)
+                sign_seed=sign_seed, status=status, replay=a.replay, device=device,
+                k_layer_max=(k_layer_max[kg].contiguous() if (k_layer_max is not None and kg
+                                                              and k_scale_mode == "tensor") else None))
             if not contiguous:
                 for j, i in enumerate(layers):
                     a.status[i] |= status[j]
@@ -474,8 +479,9 @@ class AgentCacheView:
         """All layers in one launch: list of (K, V) device tensors."""
         return self.pool.decode_layers(None, self.out_dtype)
 
-    def materialize_to_host(self, host_layers, chunk: int = 4) -> None:
-        """Decode every layer into caller-provided pinned host (K, V) tensors.
+    def materialize_to_host(self, host_layers, chunk: int = 4, layers=None) -> None:
+        """Decode every layer (or the given `layers`) into caller-provided
+        pinned host (K, V) tensors, one pair per decoded layer.
 
         Layers are decoded `chunk` at a time into two alternating device
         buffers; each chunk's device->host copy runs on a side stream while
@@ -483,7 +489,8 @@ class AgentCacheView:
         for the last copy, so a sync of it covers everything.
         """
         pool, g, dt = self.pool, self.pool.geometry, self.out_dtype
-        L = pool.num_layers
+        order = list(range(pool.num_layers)) if layers is None else list(layers)
+        L = len(order)
         if len(host_layers) != L:
             raise ValueError(f"need {L} host (K, V) pairs, got {len(host_layers)}")
         comp = torch.cuda.current_stream(pool.device)
@@ -494,7 +501,8 @@ class AgentCacheView:
                   torch.empty(g.tensor_shape, dtype=dt, device=pool.device)) for _ in range(nb)] for _ in range(2)]
         copied = [None, None]
         for c, c0 in enumerate(range(0, L, chunk)):
-            idx = list(range(c0, min(L, c0 + chunk)))
+            pos = list(range(c0, min(L, c0 + chunk)))
+            idx = [order[j] for j in pos]
             buf = bufs[c % 2][:len(idx)]
             if copied[c % 2] is not None:
                 comp.wait_event(copied[c % 2])  # the buffer's previous D2H has finished
@@ -503,7 +511,7 @@ class AgentCacheView:
             decoded.record(comp)
             copy.wait_event(decoded)
             with torch.cuda.stream(copy):
-                for (hk, hv), (dk, dv) in zip((host_layers[i] for i in idx), buf):
+                for (hk, hv), (dk, dv) in zip((host_layers[j] for j in pos), buf):
                     hk.copy_(dk, non_blocking=True)
                     hv.copy_(dv, non_blocking=True)
                 done = torch.cuda.Event()

@@ -33,8 +33,9 @@ def test_layer_and_agent_partitions():
         parallel.layer_shard(4, 2, 2)
 
 
-def fake_encode(ks, vs, g, codebook, sign_seed, k_scale_mode, device=None, check=False):
-    """Deterministic CPU stand-in for the sm_100a encoder (same arena layout)."""
+def fake_encode(ks, vs, g, codebook, sign_seed, k_scale_mode, device=None, check=False, k_layer_max=None):
+    """Deterministic CPU stand-in for the sm_100a encoder (same arena layout;
+    the key scale honours external per-layer maxima like pkv_encode)."""
     L = len(ks)
     a = _Arena(g, L, k_scale_mode, torch.device("cpu"))
     n, vecs = g.elements_per_tensor, g.vectors_per_tensor
@@ -44,13 +45,19 @@ def fake_encode(ks, vs, g, codebook, sign_seed, k_scale_mode, device=None, check
     for i, (k, v) in enumerate(zip(ks, vs)):
         kv = k.values.reshape(-1).float()
         a.k_codes[i, :n] = (kv * 50).round().clamp(-127, 127).to(torch.int8)
-        a.k_scale[i] = kv.abs().max() / 127
+        peak = kv.abs().max() if k_layer_max is None else k_layer_max[i:i + 1].view(torch.float32)[0]
+        a.k_scale[i] = (peak.to(torch.float64) / 127).to(torch.float32)
         vv = v.values.reshape(-1).float()
         a.v_packed[i, :3 * n // 8] = (vv[: 3 * n // 8] * 1000).abs().round().remainder(256).to(torch.uint8)
         a.v_scales[i, :vecs] = v.values.reshape(vecs, -1).float().pow(2).mean(-1).sqrt()
         if not bool(torch.isfinite(kv).all()):
             a.status[i] |= 1  # PKV_FLAG_K_NONFINITE, as the device encoder reports it
     return None, None, a
+
+
+def _cpu_absmax(ks, device):
+    """Test stand-in for pkv_k_absmax: max|K| bit pattern per layer (int32)."""
+    return torch.stack([k.values.abs().max().reshape(1).view(torch.int32)[0] for k in ks])
 
 
 def _geometry():
@@ -94,6 +101,20 @@ def _worker(rank, world, port, q):
             ok = False
         except pk.GeometryError as exc:
             ok = ok and "NaN or Inf" in str(exc) and "layer 4" in str(exc)
+        # head-sharded pool with the real head slicing: rank r keeps heads
+        # head_shard(3, 2, r); the per-layer key max is MAX-reduced over the
+        # ranks, so both ranks' scales are the WHOLE layer's f32(max|K|/127)
+        g3 = pk.ModelGeometry(num_layers=2, kv_heads=3, head_dim=16, seq_len=8)
+        d3 = _dump(g3)
+        hp = parallel.build_pool_head_sharded(d3, encode_fn=fake_encode, absmax_fn=_cpu_absmax)
+        hs = parallel.head_shard(3, 2, rank)
+        ok = ok and hp.head_range == hs and hp.geometry.kv_heads == len(hs)
+        for li in range(2):
+            whole = d3.layers[li][0].values.abs().max().to(torch.float64) / 127
+            ok = ok and hp.layer_blocks(li)[0].scale == float(whole.to(torch.float32))
+            mine = d3.layers[li][0].values[:, hs.start:hs.stop].reshape(-1)
+            ok = ok and torch.equal(hp.layer_blocks(li)[0].codes.reshape(-1), (mine * 50).round().clamp(-127, 127)
+                                    .to(torch.int8))
         q_ok = ok
     except Exception as exc:  # noqa: BLE001
         q_ok = repr(exc)
