@@ -185,6 +185,23 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim,
                          void* workspace, size_t workspace_bytes,
                          void* stream);
 
+/*
+ * pkv_layer_stats — build statistics of `num_layers` layers (LayerStats,
+ * kvpool/pool.py:274-288, metrics.py:166-222) in one fused f64 reduction:
+ * out[4*l + 0..3] = { sum (Kdec-K)^2, max |Kdec-K|, sum (Vdec-V)^2, sum V^2 }
+ * over the `count` elements of layer l (double, device). k_in / v_in: the
+ * source tensors (f32 or bf16, `in_dtype`); k_dec / v_dec: the f32 decode of
+ * the pool (pkv_decode at PKV_F32 == the reference's 32-bit decode).
+ * Deterministic (fixed reduction order). workspace: device scratch of
+ * pkv_layer_stats_workspace_bytes(num_layers, count).
+ */
+size_t pkv_layer_stats_workspace_bytes(int num_layers, int64_t count);
+int pkv_layer_stats(int num_layers, int64_t count, int in_dtype,
+                    const void* const* k_in, const void* const* v_in,
+                    const float* const* k_dec, const float* const* v_dec,
+                    double* out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* Internal self-checks that need the device. PKV_SELFTEST_DIVISION runs the
  * decode kernel's correctly-rounded x / f32(sqrt(d)) sequence for d in
  * {8, 32, 128} and the block32 key-scale x / 127 sequence against IEEE

@@ -335,3 +335,39 @@ def attention_over_pool(q: np.ndarray, k_deq: np.ndarray, v_deq: np.ndarray,
             p /= p.sum(axis=-1, keepdims=True)
             out[r, h] = p @ v
     return out
+
+
+# ---------------------------------------------------------------------------
+# PKVP v1 snapshots (pool.py:14-25, 57-63, 301-432)
+# ---------------------------------------------------------------------------
+
+PKVP_HEADER = "<4sHHIIIIIHQ6x"  # magic, version, flags, L, B, H, T, D, baseline_bits, sign seed (44 bytes)
+
+
+def read_pkvp(data: bytes) -> dict:
+    """Parse a PKVP v1 file: per layer f32 key scale, int8 key codes, f32
+    value scales, then uint8 value codes (flag 0x1: packed 8 codes / 3 bytes)."""
+    import struct
+
+    magic, version, flags, L, B, H, T, D, bits, seed = struct.unpack_from(PKVP_HEADER, data, 0)
+    if magic != b"PKVP" or version != 1:
+        raise ValueError("not a PKVP v1 file")
+    e, vecs = B * H * T * D, B * H * T
+    packed = bool(flags & 0x1)
+    off = struct.calcsize(PKVP_HEADER)
+    layers = []
+    for _ in range(L):
+        (scale,) = struct.unpack_from("<f", data, off)
+        off += 4
+        kc = np.frombuffer(data, np.int8, e, off).reshape(B, H, T, D)
+        off += e
+        vs = np.frombuffer(data, "<f4", vecs, off).reshape(B, H, T).astype(np.float32)
+        off += 4 * vecs
+        nv = 3 * ((e + 7) // 8) if packed else e
+        raw = np.frombuffer(data, np.uint8, nv, off)
+        off += nv
+        vc = (unpack3(raw, e) if packed else raw.copy()).reshape(B, H, T, D)
+        layers.append((float(scale), kc.copy(), vc, vs))
+    if off != len(data):
+        raise ValueError(f"{len(data) - off} trailing bytes")
+    return {"geom": (L, B, H, T, D), "flags": flags, "sign_seed": seed if flags & 0x2 else None, "layers": layers}

@@ -49,6 +49,9 @@ SIGNATURES: dict[str, tuple] = {
          c_void_p, c_void_p, c_void_p, c_size, c_void_p],
     ),
     "pkv_k_absmax": (c_int, [c_int, c_i64, c_int, P(c_void_p), c_void_p, c_void_p]),
+    "pkv_layer_stats_workspace_bytes": (c_size, [c_int, c_i64]),
+    "pkv_layer_stats": (c_int, [c_int, c_i64, c_int, P(c_void_p), P(c_void_p), P(c_void_p), P(c_void_p), c_void_p,
+                                c_void_p, c_size, c_void_p]),
     "pkv_decode": (
         c_int,
         [c_int, c_i64, c_int, c_int, c_int, P(c_void_p), P(c_void_p), P(c_void_p), P(c_void_p),

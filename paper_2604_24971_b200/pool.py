@@ -622,22 +622,44 @@ def attach_agent(pool: SharedPool, decode_bits: int = 16) -> AgentCacheView:
     return pool.attach(decode_bits)
 
 
-def compute_layer_stats(dump: KvDump, pool: SharedPool) -> tuple:
-    """LayerStats (pool.py:274-288): f32 decode on the GPU, f64 error reductions."""
+def compute_layer_stats(dump: KvDump, pool: SharedPool, chunk: int = 8) -> tuple:
+    """LayerStats (pool.py:274-288): the f32 decode of the pool (pkv_decode,
+    == the reference's 32-bit dequantize_k / dequantize_v) and one fused f64
+    error reduction (pkv_layer_stats), `chunk` layers at a time."""
+    from ._lib import check, load, ptr_array
+
+    g = pool.geometry
+    n = g.elements_per_tensor
+    dev = pool.device
+    L = pool.num_layers
+    lib = load()
+    sums = torch.empty((L, 4), dtype=torch.float64, device=dev)
+    ws_bytes = lib.pkv_layer_stats_workspace_bytes(min(L, chunk), n)
+    ws = torch.empty((ws_bytes + 7) // 8, dtype=torch.float64, device=dev)
+    for c0 in range(0, L, chunk):
+        idx = list(range(c0, min(L, c0 + chunk)))
+        decoded = pool.decode_layers(idx, torch.float32)
+        ks = _device_inputs([dump.layers[i][0] for i in idx], dev)
+        vs = _device_inputs([dump.layers[i][1] for i in idx], dev)
+        dt = {t.dtype for t in ks + vs}
+        if len(dt) != 1 or dt.pop() not in (torch.float32, torch.bfloat16):
+            ks = [t.float() for t in ks]
+            vs = [t.float() for t in vs]
+        rc = lib.pkv_layer_stats(
+            len(idx), n, _codec.dtype_code(ks[0]), ptr_array([t.data_ptr() for t in ks]),
+            ptr_array([t.data_ptr() for t in vs]), ptr_array([k.data_ptr() for k, _ in decoded]),
+            ptr_array([v.data_ptr() for _, v in decoded]), sums[c0].data_ptr(), ws.data_ptr(),
+            ws.numel() * 8, _codec.stream_ptr(dev))
+        check(rc, "pkv_layer_stats")
+    host = sums.cpu().numpy()
     stats = []
-    decoded = pool.decode_layers(None, torch.float32)
-    for idx, ((k, v), (kd, vd)) in enumerate(zip(dump.layers, decoded)):
+    for idx in range(L):
+        sk, kmax, sv, sp = (float(x) for x in host[idx])
         kq, _ = pool.layer_blocks(idx)
-        kref = k.values.to(pool.device, torch.float64)
-        vref = v.values.to(pool.device, torch.float64)
-        kerr = kd.to(torch.float64) - kref
-        verr = vd.to(torch.float64) - vref
-        v_power = float(torch.mean(vref * vref))
-        v_mse = float(torch.mean(verr * verr))
-        stats.append(LayerStats(
-            layer=idx, k_scale=kq.scale, k_mse=float(torch.mean(kerr * kerr)),
-            k_max_err=float(kerr.abs().max()), v_mse=v_mse,
-            v_nmse=v_mse / v_power if v_power > 0.0 else 0.0))
+        v_mse = sv / n
+        v_power = sp / n
+        stats.append(LayerStats(layer=idx, k_scale=kq.scale, k_mse=sk / n, k_max_err=kmax, v_mse=v_mse,
+                                v_nmse=v_mse / v_power if v_power > 0.0 else 0.0))
     return tuple(stats)
 
 
