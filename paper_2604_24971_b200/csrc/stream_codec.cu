@@ -311,8 +311,27 @@ __device__ __noinline__ void v_replay(const EncArgs& a, const TIn* src, uint8_t*
   const double sq = sqrt((double)D);  // fwht.py:50
   for (int i = lane; i < D; i += 32) R[i] = R[i] / sq;
   __syncwarp();
+  // np.mean(np.square(rot)) (valuequant.py:207) in numpy's pairwise order
+  // (pkv_common.cuh:pairwise_sumsq): for D <= 128 the eight interleaved
+  // accumulators r[j] run on lanes 0..7, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+  // by butterflies (IEEE addition is commutative, so the xor partners give
+  // lane 0 exactly numpy's result).
+  double sum;
+  if constexpr (D >= 8 && D <= 128) {
+    double acc = 0.0;
+    if (lane < 8) {
+      acc = sq_rn(R[lane]);
+      for (int i = 8 + lane; i < D; i += 8) acc = __dadd_rn(acc, sq_rn(R[i]));
+    }
+    acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    sum = acc;
+  } else {
+    sum = lane == 0 ? pairwise_sumsq(R, D) : 0.0;
+  }
   double rms = 0.0;
-  if (lane == 0) rms = sqrt(pairwise_sumsq(R, D) / (double)D);  // valuequant.py:207
+  if (lane == 0) rms = sqrt(sum / (double)D);
   rms = __shfl_sync(0xffffffffu, rms, 0);
   const float scale = (float)rms;  // valuequant.py:208
   const double den = rms > 0.0 ? rms : 1.0;
@@ -337,6 +356,39 @@ __device__ __noinline__ void v_replay(const EncArgs& a, const TIn* src, uint8_t*
     if (a.replay_count) atomicAdd(a.replay_count, 1u);
   }
   __syncwarp();
+}
+
+// rsqrt.approx.f64: ~2^-22 relative seed for the Newton steps below
+__device__ __forceinline__ double rsqrt_seed(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// The f32 value scale RN32(sqrt(S / D)) (valuequant.py:207-208) from the
+// fp64 sum of squares S in [2^-200, 2^200], without an fp64 square root:
+// r = T * y with T = S / D (exact) and y = 1/sqrt(T) from the rsqrt seed and
+// two Newton steps (relative error of r < 2^-48, S itself is within
+// D * 2^-53 of numpy's sum). The f32 rounding of r is trusted when r is
+// farther than 2^-40 * r from the f32 rounding boundary on its side of
+// c = RN32(r); otherwise returns false and the vector is replayed in numpy's
+// exact order. Also N = ||x|| = sqrt(D) * r in f32 (for the code
+// thresholds; its error is inside the guard band, guard_delta()).
+template <int D>
+__device__ __forceinline__ bool scale_from_sumsq(double S, float& scale, float& N) {
+  const double T = S * (1.0 / D);
+  double y = rsqrt_seed(T);
+  y = y * fma(-0.5 * T, y * y, 1.5);
+  y = y * fma(-0.5 * T, y * y, 1.5);
+  const double r = T * y;
+  const float c = __double2float_rn(r);
+  const double cd = (double)c;
+  const uint32_t cb = __float_as_uint(c);
+  const double gap = r >= cd ? (double)__uint_as_float(cb + 1u) - cd : cd - (double)__uint_as_float(cb - 1u);
+  const double dist = 0.5 * gap - fabs(r - cd);  // to the rounding boundary between c and its neighbour
+  scale = c;
+  N = __double2float_rn(r * (D == 64 ? 8.0 : D == 16 ? 4.0 : D == 128 ? 11.313708498984761 : 5.656854249492381));
+  return dist > 0x1p-40 * r;
 }
 
 // pack NW 24-bit words (chunk order) and store them at global address `dst`
@@ -433,13 +485,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
     } else if (S < 0x1p-200 || S > 0x1p+200) {
       replay = true;
     } else {
-      const double rr = sqrt(S * (1.0 / D));  // S/D is exact (D = 2^k)
-      scale = (float)rr;
-      const double fd = (double)scale;
-      const float nb = (rr >= fd) ? nextafterf(scale, INFINITY) : nextafterf(scale, 0.f);
-      const double half_ulp = fabs((double)nb - fd) * 0.5;
-      if (half_ulp - fabs(rr - fd) <= 1e-12 * rr) replay = true;  // f32 rounding of the scale in doubt
-      N = (float)sqrt(S);  // ||x||; z = U / ||x||
+      replay = !scale_from_sumsq<D>(S, scale, N);  // f32 rounding of the scale in doubt -> exact replay
     }
 
     uint32_t words[NCL];
