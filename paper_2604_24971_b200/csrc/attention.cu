@@ -335,6 +335,355 @@ __global__ void __launch_bounds__(kAttnThreads2, 2) prefix_kernel2(const __grid_
   }
 }
 
+// ---------------------------------------------------------------------------
+// prefix kernel, tensor-core version (mma.sync m16n8k16, f16 in / f32 acc)
+// ---------------------------------------------------------------------------
+// Same split / partial layout as prefix_kernel2 (the combine kernel is
+// shared), but S = Q K^T and O += P Y run on the tensor cores. Precision:
+//   * K codes are integers |c| <= 128: exact in f16; the per-tensor key
+//     scale is applied to S in f32 after the MMA (block32: f16(code * s16));
+//   * Q (pre-scaled by softmax_scale * log2 e) is split hi + lo in f16
+//     (two MMAs, ~2^-22 relative), so large logits keep f32-like accuracy;
+//   * the rotated-domain values Y = centroid[code] * rms are factored:
+//     rms scales P (per token, f32) and the centroids are split hi + lo in
+//     f16 (two MMAs): the centroid rounding is systematic across tokens and
+//     would not average out;
+//   * P' = p * rms is rounded to f16 (random per token).
+// CTA = 4 warps; WR warps along rows (16 rows each), 4 / WR along the
+// tokens of each 64-token tile (rows <= 16: WR = 1, the four warps split
+// the tile and merge their online-softmax states at the end).
+namespace mma {
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+// f32 pair -> (hi, lo) f16 pairs with hi + lo == x to ~2^-22
+__device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 hf = __half22float2(h);
+  hi = h2u(h);
+  lo = h2u(__floats2half2_rn(x - hf.x, y - hf.y));
+}
+// byte offset of 16-byte chunk c of row r in a [rows][D] f16 tile, XOR-swizzled
+// so that ldmatrix reads of 8 consecutive rows hit 8 distinct chunk slots
+template <int D>
+__device__ __forceinline__ uint32_t sw(int r, int c) {
+  return (uint32_t)(r * (2 * D) + ((c ^ (r & 7)) << 4));
+}
+
+template <int D, int WR>
+struct MmaTile {
+  static constexpr int RT = 16 * WR;            // rows per CTA
+  static constexpr int WT = 4 / WR;             // warps along tokens
+  static constexpr int TT = 64;                 // tokens per tile
+  static constexpr int TW = TT / WT;            // tokens per warp per tile
+  static constexpr int Q_BYTES = RT * D * 2;    // one f16 Q tile (hi or lo)
+  static constexpr int T_BYTES = TT * D * 2;    // one f16 K / Y tile
+  static constexpr int RAW = TT * D + TT * 3 * D / 8 + TT * 4;
+  static constexpr int MERGE = WT > 1 ? 4 * 16 * (D + 2) * 4 : 0;  // every warp's 16-row state
+  static constexpr int MAIN = 2 * Q_BYTES + 3 * T_BYTES + TT * 4 + RAW;
+  static constexpr int SMEM = (MAIN > MERGE ? MAIN : MERGE) + 128 * 8 * 4 + 128;
+};
+
+}  // namespace mma
+
+template <int D, int WR>
+__global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a) {
+  using namespace mma;
+  using MT = MmaTile<D, WR>;
+  constexpr int RT = MT::RT, WT = MT::WT, TT = MT::TT, TW = MT::TW;
+  constexpr int NB = TW / 8;   // S n-blocks (8 tokens) per warp per tile
+  constexpr int KS = D / 16;   // k-steps of S
+  constexpr int ND = D / 8;    // O n-blocks (8 dims)
+  extern __shared__ __align__(128) uint8_t smm[];
+  uint8_t* qhi = smm;
+  uint8_t* qlo = qhi + MT::Q_BYTES;
+  uint8_t* kh = qlo + MT::Q_BYTES;
+  uint8_t* yhi = kh + MT::T_BYTES;
+  uint8_t* ylo = yhi + MT::T_BYTES;
+  float* rms_s = reinterpret_cast<float*>(ylo + MT::T_BYTES);
+  uint8_t* raw = reinterpret_cast<uint8_t*>(rms_s + TT);
+  int8_t* rk = reinterpret_cast<int8_t*>(raw);
+  uint8_t* rv = raw + TT * D;
+  float* rs = reinterpret_cast<float*>(raw + TT * D + TT * 3 * D / 8);
+  // per-thread (conflict-free) table: code -> (centroid hi, centroid lo) f16 bits
+  uint32_t* ctab = reinterpret_cast<uint32_t*>(smm + (MT::MAIN > MT::MERGE ? MT::MAIN : MT::MERGE));
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp % WR, wt = warp / WR;  // row block, token slice
+  const int h = blockIdx.y, sp = blockIdx.x, r0 = blockIdx.z * RT;
+  const long long tiles = (a.T + TT - 1) / TT;
+  const long long per = (tiles + a.splits - 1) / a.splits * TT;
+  const long long t_begin = (long long)sp * per, t_end = min(a.T, t_begin + per);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __half hc = __float2half_rn(a.cent32[k]);
+    const __half lc = __float2half_rn(a.cent32[k] - __half2float(hc));
+    ctab[k * 128 + tid] = (uint32_t)__half_as_ushort(hc) | ((uint32_t)__half_as_ushort(lc) << 16);
+  }
+  // ---- Q tile (x qscale), split hi / lo, f16 swizzled [RT][D] ----
+  for (int i = tid; i < RT * D / 8; i += 128) {
+    const int r = i / (D / 8), c = i % (D / 8);
+    const int row = r0 + r;
+    float qv[8];
+    if (row < a.rows) {
+      const int agent = row / a.group, g = row % a.group;
+      const long long off = (((long long)agent * a.kv_heads + h) * a.group + g) * D + c * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qv[j] = ldq(a, off + j) * a.qscale;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qv[j] = 0.f;
+    }
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) split2(qv[2 * j], qv[2 * j + 1], hi[j], lo[j]);
+    *reinterpret_cast<uint4*>(qhi + sw<D>(r, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(qlo + sw<D>(r, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+  const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 1.f;
+
+  auto stage = [&](long long t0, int nt) {
+    const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
+    for (int i = tid; i < nt * D / 16; i += 128) cp_async16(rk + i * 16, gk + i * 16);
+    const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
+    for (int i = tid; i < nt * (3 * D / 8) / 4; i += 128) cp_async4(rv + i * 4, gv + i * 4);
+    const float* gs = a.v_scales + (long long)h * a.T + t0;
+    for (int i = tid; i < nt; i += 128) cp_async4(rs + i, gs + i);
+    cp_async_commit();
+  };
+  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT, t_end - t_begin));
+
+  float o[ND][4];
+#pragma unroll
+  for (int j = 0; j < ND; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // rows g, g + 8
+  const int g = lane >> 2, t4 = lane & 3;
+  const uint32_t qhi_s = (uint32_t)__cvta_generic_to_shared(qhi), qlo_s = (uint32_t)__cvta_generic_to_shared(qlo);
+  const uint32_t kh_s = (uint32_t)__cvta_generic_to_shared(kh);
+  const uint32_t yhi_s = (uint32_t)__cvta_generic_to_shared(yhi), ylo_s = (uint32_t)__cvta_generic_to_shared(ylo);
+  const int qrow = wr * 16;
+
+  for (long long t0 = t_begin; t0 < t_end; t0 += TT) {
+    const int nt = (int)min((long long)TT, t_end - t0);
+    cp_async_wait_all();
+    __syncthreads();  // raw tile landed; every warp is done with the previous K / Y tiles
+    // ---- K: int8 codes -> f16 (exact; block32: x f16 scale), 16 codes per thread-step ----
+    for (int i = tid; i < TT * D / 16; i += 128) {
+      const int t = i / (D / 16), c = i % (D / 16);
+      uint4 w = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // code 0
+      __half2 sc2 = __float2half2_rn(1.f);
+      if (t < nt) {
+        w = *reinterpret_cast<const uint4*>(rk + t * D + c * 16);
+        w.x ^= 0x80808080u; w.y ^= 0x80808080u; w.z ^= 0x80808080u; w.w ^= 0x80808080u;
+        if (a.k_mode != PKV_K_TENSOR)
+          sc2 = __half2half2(a.k_bscale[(((long long)h * a.T + t0 + t) * D + c * 16) >> 5]);
+      }
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      const __half2 bias = __float2half2_rn(1152.f);  // 1024 + 128
+      uint32_t hv[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __half2 lo2 = __hsub2(u2h(__byte_perm(ww[j], 0x64646464u, 0x5140)), bias);
+        __half2 hi2 = __hsub2(u2h(__byte_perm(ww[j], 0x64646464u, 0x7362)), bias);
+        if (a.k_mode != PKV_K_TENSOR) {
+          lo2 = __hmul2(lo2, sc2);
+          hi2 = __hmul2(hi2, sc2);
+        }
+        hv[2 * j] = h2u(lo2);
+        hv[2 * j + 1] = h2u(hi2);
+      }
+      *reinterpret_cast<uint4*>(kh + sw<D>(t, 2 * c)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<uint4*>(kh + sw<D>(t, 2 * c + 1)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+    }
+    // ---- V: 3-bit codes -> centroid hi / lo f16 tiles; rms per token ----
+    for (int i = tid; i < TT * D / 8; i += 128) {
+      const int t = i / (D / 8), c = i % (D / 8);
+      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+      if (t < nt) {
+        const uint8_t* p = rv + t * (3 * D / 8) + 3 * c;
+        const uint32_t word = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const uint32_t x0 = ctab[((word >> (3 * e)) & 7u) * 128 + tid];
+          const uint32_t x1 = ctab[((word >> (3 * e + 3)) & 7u) * 128 + tid];
+          hi[e / 2] = __byte_perm(x0, x1, 0x5410);
+          lo[e / 2] = __byte_perm(x0, x1, 0x7632);
+        }
+      }
+      *reinterpret_cast<uint4*>(yhi + sw<D>(t, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(ylo + sw<D>(t, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    for (int i = tid; i < TT; i += 128) rms_s[i] = i < nt ? rs[i] : 0.f;
+    __syncthreads();  // tiles converted; raw buffer free
+    if (t0 + TT < t_end) stage(t0 + TT, (int)min((long long)TT, t_end - t0 - TT));
+
+    // ---- S = Q K^T over this warp's TW tokens ----
+    const int tw0 = wt * TW;
+    float s[NB][4];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      uint32_t ah[4], al[4];
+      const int ar = qrow + (lane & 7) + 8 * ((lane >> 3) & 1), ac = 2 * k + (lane >> 4);
+      ldsm_x4(qhi_s + sw<D>(ar, ac), ah);
+      ldsm_x4(qlo_s + sw<D>(ar, ac), al);
+#pragma unroll
+      for (int n = 0; n < NB; n += 2) {
+        uint32_t b[4];
+        const int br = tw0 + n * 8 + (lane & 7) + 8 * (lane >> 4), bc = 2 * k + ((lane >> 3) & 1);
+        ldsm_x4(kh_s + sw<D>(br, bc), b);
+        mma16816(s[n], ah, b[0], b[1]);
+        mma16816(s[n], al, b[0], b[1]);
+        if (n + 1 < NB) {
+          mma16816(s[n + 1], ah, b[2], b[3]);
+          mma16816(s[n + 1], al, b[2], b[3]);
+        }
+      }
+    }
+    // ---- online softmax (rows g and g + 8 of this warp's 16) ----
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int n = 0; n < NB; ++n)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int tok = tw0 + n * 8 + 2 * t4 + (j & 1);
+        s[n][j] = tok < nt ? s[n][j] * ts : -INFINITY;
+        mx[j >> 1] = fmaxf(mx[j >> 1], s[n][j]);
+      }
+    float corr[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], 1));
+      mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], 2));
+      const float m_new = fmaxf(m_run[rr], mx[rr]);
+      // a slice with no tokens yet (m_new = -inf) keeps everything at 0
+      corr[rr] = m_new == -INFINITY ? 1.f : exp2f(m_run[rr] - m_new);
+      m_run[rr] = m_new;
+    }
+    float lsum[2] = {0.f, 0.f};
+    uint32_t pa[NB][2];  // P' = p * rms as f16 pairs: [n][row g / g + 8]
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const int tok = tw0 + n * 8 + 2 * t4;
+      const float2 rm = *reinterpret_cast<const float2*>(rms_s + tok);
+      float p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float m = m_run[j >> 1];
+        p[j] = m == -INFINITY ? 0.f : exp2f(s[n][j] - m);
+        lsum[j >> 1] += p[j];
+      }
+      pa[n][0] = h2u(__floats2half2_rn(p[0] * rm.x, p[1] * rm.y));
+      pa[n][1] = h2u(__floats2half2_rn(p[2] * rm.x, p[3] * rm.y));
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      lsum[rr] += __shfl_xor_sync(0xffffffffu, lsum[rr], 1);
+      lsum[rr] += __shfl_xor_sync(0xffffffffu, lsum[rr], 2);
+      l_run[rr] = l_run[rr] * corr[rr] + lsum[rr];
+    }
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      o[j][0] *= corr[0]; o[j][1] *= corr[0];
+      o[j][2] *= corr[1]; o[j][3] *= corr[1];
+    }
+    // ---- O += P' (Y_hi + Y_lo) over the warp's tokens, 16 tokens per k-step ----
+#pragma unroll
+    for (int kk = 0; kk < TW / 16; ++kk) {
+      const uint32_t af[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+      const int br = tw0 + kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+#pragma unroll
+      for (int j = 0; j < ND; j += 2) {
+        uint32_t bh[4], bl[4];
+        const int bc = j + (lane >> 4);
+        ldsm_x4_t(yhi_s + sw<D>(br, bc), bh);
+        ldsm_x4_t(ylo_s + sw<D>(br, bc), bl);
+        mma16816(o[j], af, bh[0], bh[1]);
+        mma16816(o[j], af, bl[0], bl[1]);
+        mma16816(o[j + 1], af, bh[2], bh[3]);
+        mma16816(o[j + 1], af, bl[2], bl[3]);
+      }
+    }
+  }
+
+  // ---- partials: [h][split][row][0..D) acc, D: m, D+1: l ----
+  if constexpr (WT > 1) {
+    __syncthreads();  // tiles no longer needed: reuse shared memory to merge the token slices
+    float* mrg = reinterpret_cast<float*>(smm);
+    float* mine = mrg + (wt * WR + wr) * 16 * (D + 2);  // [token slice][row block][16 rows][D + 2]
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+      const int c = j * 8 + 2 * t4;
+      mine[g * (D + 2) + c] = o[j][0];
+      mine[g * (D + 2) + c + 1] = o[j][1];
+      mine[(g + 8) * (D + 2) + c] = o[j][2];
+      mine[(g + 8) * (D + 2) + c + 1] = o[j][3];
+    }
+    if (t4 == 0) {
+      mine[g * (D + 2) + D] = m_run[0];
+      mine[g * (D + 2) + D + 1] = l_run[0];
+      mine[(g + 8) * (D + 2) + D] = m_run[1];
+      mine[(g + 8) * (D + 2) + D + 1] = l_run[1];
+    }
+    __syncthreads();
+    // 128 threads: thread -> (row of the RT-row tile, column)
+    for (int i = tid; i < RT * (D + 2); i += 128) {
+      const int r = i / (D + 2), c = i % (D + 2);
+      const int row = r0 + r;
+      if (row >= a.rows || c == D + 1) continue;
+      const float* st = mrg + ((r >> 4) * 16 + (r & 15)) * (D + 2);  // slice 0, row block r / 16
+      constexpr int SL = WR * 16 * (D + 2);                          // stride between token slices
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < WT; ++w) M = fmaxf(M, st[w * SL + D]);
+      float* dst = a.part + (((long long)h * a.splits + sp) * a.rows + row) * (D + 4);
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < WT; ++w) {
+        const float mw = st[w * SL + D];
+        v += mw == -INFINITY ? 0.f : exp2f(mw - M) * st[w * SL + (c == D ? D + 1 : c)];
+      }
+      if (c == D) {
+        dst[D] = M;
+        dst[D + 1] = v;
+      } else {
+        dst[c] = v;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int row = r0 + qrow + g + 8 * rr;
+      if (row >= a.rows) continue;
+      float* dst = a.part + (((long long)h * a.splits + sp) * a.rows + row) * (D + 4);
+#pragma unroll
+      for (int j = 0; j < ND; ++j)
+        *reinterpret_cast<float2*>(dst + j * 8 + 2 * t4) = make_float2(o[j][2 * rr], o[j][2 * rr + 1]);
+      if (t4 == 0) {
+        dst[D] = m_run[rr];
+        dst[D + 1] = l_run[rr];
+      }
+    }
+  }
+}
+
 // One CTA of kCombineWarps warps per (row, kv head): the warps merge
 // interleaved subsets of the splits, warp 0 folds their results, then
 // inverse-rotates and adds the private tail.
@@ -533,8 +882,27 @@ int launch_rt(Args& a, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
 
+template <int D, int WR>
+int launch_mma(Args& a, cudaStream_t st) {
+  using MT = mma::MmaTile<D, WR>;
+  if (cudaFuncSetAttribute(prefix_mma<D, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MT::SMEM) !=
+      cudaSuccess)
+    return PKV_ERR_CUDA;
+  const int row_tiles = (a.rows + MT::RT - 1) / MT::RT;
+  dim3 grid(a.splits, a.kv_heads, row_tiles);
+  prefix_mma<D, WR><<<grid, 128, MT::SMEM, st>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
+  combine_kernel<D><<<a.rows * a.kv_heads, 32 * kCombineWarps, 0, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+}
+
 template <int D>
 int launch(Args& a, cudaStream_t st) {
+  if (!tuning().attn_simt) {  // tensor-core prefix (default)
+    if (a.rows <= 16) return launch_mma<D, 1>(a, st);
+    if (a.rows <= 32) return launch_mma<D, 2>(a, st);
+    return launch_mma<D, 4>(a, st);
+  }
   return a.rows <= 16 ? launch_rt<D, 16>(a, st) : launch_rt<D, 64>(a, st);
 }
 

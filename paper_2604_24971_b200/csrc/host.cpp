@@ -24,6 +24,7 @@ Tuning read_env() {
   if (const char* e = std::getenv("PKV_KEY_SM_FRACTION")) t.key_sm_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_DEC_KEY_FRACTION")) t.dec_key_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM")) t.attn_ctas_per_sm = std::atoi(e);
+  if (const char* e = std::getenv("PKV_ATTN_PATH")) t.attn_simt = std::strcmp(e, "simt") == 0;
   return t;
 }
 std::mutex g_reload;

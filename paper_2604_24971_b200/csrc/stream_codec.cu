@@ -185,6 +185,14 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// acquire pattern for a relaxed read that observed a release (PTX memory
+// model: observation + fence.acq_rel synchronizes with red.release)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1229,14 +1237,27 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         const uint32_t nA = (uint32_t)a.nA, nE = (uint32_t)a.nE;
         const uint32_t totA = (uint32_t)a.num_layers * nA, totE = (uint32_t)a.num_layers * nE;
         uint32_t ta = (uint32_t)role_rank, te = (uint32_t)role_rank;
-        int ready = -1;  // layers [0, ready] staged in ctl->layer_max
+        int ready = -1;      // layers [0, ready] staged in ctl->layer_max
         int polled = -1;     // layer whose count is in `polled_cnt`
         uint32_t polled_cnt = 0;
-        auto stage = [&](int l) {
-          ctl->layer_max[l] = *reinterpret_cast<volatile const uint32_t*>(a.layer_max + l);
+        int pending = -1;    // layer whose max is in flight in `pending_max`
+        uint32_t pending_max = 0;
+        // Every global read here is RELAXED and consumed one call later, so
+        // its L2 round trip overlaps the TMA issues in between (an ld.acquire
+        // holds back the bulk copies issued after it). Acquire ordering is
+        // established once per layer: a
+        // relaxed read that sees the complete count (written with
+        // red.release) followed by fence.acq_rel, then the max is read.
+        auto stage = [&](int l, uint32_t mx) {
+          ctl->layer_max[l] = mx;
           __threadfence_block();
           *reinterpret_cast<volatile uint32_t*>(&ctl->ready[l]) = 1u;
           ready = l;
+        };
+        auto request_max = [&](int l) {
+          fence_acq_rel_gpu();
+          pending_max = ld_relaxed_u32(a.layer_max + l);  // consumed at the next call
+          pending = l;
         };
         auto next_item = [&]() -> Item {
           for (;;) {
@@ -1247,25 +1268,32 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
               te += G;
               return it;
             }
-            if (polled == el && polled_cnt >= nA) {
-              stage(el);
+            if (pending == el) {
+              stage(el, pending_max);
               continue;
             }
-            polled = el;
-            polled_cnt = ld_acquire_u32(a.layer_done + el);  // consumed at the next call
+            if (polled == el && polled_cnt >= nA) {
+              request_max(el);
+            } else {
+              polled = el;
+              polled_cnt = ld_relaxed_u32(a.layer_done + el);  // consumed at the next call
+            }
             if (ta < totA && (int)(ta / nA) < el + a.key_lag) {
               const int al = (int)(ta / nA);
               const Item it{kAbsmax, al, (int)(ta - (uint32_t)al * nA), 0};
               ta += G;
               return it;
             }
-            uint32_t spins = 0;
-            uint64_t t0 = 0;
-            while (ld_acquire_u32(a.layer_done + el) < nA) {
-              __nanosleep(128);
-              tma::watchdog(spins, t0);
+            if (pending != el) {  // nothing else to issue: wait for layer el's absmax items
+              uint32_t spins = 0;
+              uint64_t t0 = 0;
+              while (ld_relaxed_u32(a.layer_done + el) < nA) {
+                __nanosleep(128);
+                tma::watchdog(spins, t0);
+              }
+              request_max(el);
             }
-            stage(el);
+            stage(el, pending_max);
           }
         };
         produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);

@@ -16,6 +16,7 @@ struct Tuning {
   double key_sm_fraction = -1.0;   // PKV_KEY_SM_FRACTION (<0 = default): encode SMs for the key role
   double dec_key_fraction = -1.0;  // PKV_DEC_KEY_FRACTION (<0 = default): decode SMs for key items
   int attn_ctas_per_sm = 0;        // PKV_ATTN_CTAS_PER_SM (0 = default): attention prefix splits
+  bool attn_simt = false;          // PKV_ATTN_PATH=simt: fp32 CUDA-core prefix kernel instead of mma.sync
 };
 
 // The current knobs (an immutable snapshot; cheap to call per launch).

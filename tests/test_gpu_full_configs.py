@@ -165,3 +165,38 @@ def test_attention_at_bench_shapes_vs_oracle_decode(T):
 def test_attention_block32_keys_and_sign_diagonal(k_mode, sign_seed):
     rel = attention_case(1000, agents=5, k_mode=k_mode, sign_seed=sign_seed)
     assert rel < 1e-3, rel
+
+
+@pytest.mark.parametrize("shape", [(8, 128, 4096, 15, 4), (32, 64, 1851, 5, 1), (8, 128, 300, 3, 4), (4, 64, 700, 9, 2)],
+                         ids=lambda s: "h%d_d%d_t%d_a%d_g%d" % s)
+@pytest.mark.parametrize("qmul", [1.0, 40.0], ids=["logits1", "logits40"])
+def test_tensor_core_attention_matches_oracle_and_simt(monkeypatch, shape, qmul):
+    """The mma.sync prefix kernel (default) against the fp64 oracle over the
+    oracle's decode, at ordinary and at large logits (q x 40: the split-f16 Q
+    keeps the logit error ~2^-22 relative), and against the fp32 CUDA-core
+    kernel (PKV_ATTN_PATH=simt)."""
+    from paper_2604_24971_b200 import _lib
+    from paper_2604_24971_b200 import attention as A
+
+    H, D, T, R, G = shape
+    g = pk.ModelGeometry(num_layers=1, kv_heads=H, head_dim=D, seq_len=T)
+    host = O.synth_dump(1, H, D, T, seed=17)
+    dump = device_dump(g, host, torch.float32)
+    pool = pk.build_pool(dump, build_stats=False)
+    w = check_pool_layers(pool, dump, [0])[0]
+    kd, vd = O.decode_layer(w["k_codes"], w["k_scale"], w["v_codes"], w["v_scales"], 32)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn(R, H, G, D, device="cuda", generator=gen) * qmul
+    want = O.attention_over_pool(q.cpu().numpy(), kd[0], vd[0], D ** -0.5)
+    got = A.decode_attention(pool, 0, q, softmax_scale=D ** -0.5, out_dtype=torch.float32).cpu().numpy()
+    rel = np.abs(got - want).max() / np.abs(want).max()
+    assert rel < 1e-3, rel
+    monkeypatch.setenv("PKV_ATTN_PATH", "simt")
+    _lib.reload_tuning()
+    try:
+        simt = A.decode_attention(pool, 0, q, softmax_scale=D ** -0.5, out_dtype=torch.float32).cpu().numpy()
+    finally:
+        monkeypatch.undo()
+        _lib.reload_tuning()
+    assert np.abs(simt - want).max() / np.abs(want).max() < 1e-3
+    assert np.abs(got - simt).max() / np.abs(want).max() < 1e-3
