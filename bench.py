@@ -545,12 +545,13 @@ def run_ours(args, cfg):
             a_ms = s2.elapsed_time(e2) / args.steps
         a_ms = max_over_ranks(a_ms)
         pool_bytes = L * (n * (1 + 3 / 8) + 4 * vecs + 4)
-        flops = 4.0 * L * agents * group * T * D  # q.k and p.v per query row, all layers
+        flops = 4.0 * L * agents * H * group * T * D  # q.k and p.v for every query row of every head and layer
         attn = {"tokens_per_s": agents / (a_ms / 1e3), "ms_per_token_step": a_ms, "agents": agents,
                 "agents_per_rank": len(my_agents), "layers": L,
                 "scope": "attention only (all layers), each rank batches its agents over its pool replica",
                 "pool_gbs_per_rank": pool_bytes / (a_ms / 1e3) / 1e9,
-                "tflops": flops / (a_ms / 1e3) / 1e12 if world == 1 else None}
+                "tflops": flops / (a_ms / 1e3) / 1e12 if world == 1 else None,
+                "kernel": "prefix (mma.sync f16 / f32 acc, split-f16 Q and centroids) + combine"}
 
     # ---- model-level shared-pool decode (random-init model of the config's shape) ----
     dec_e2e = None

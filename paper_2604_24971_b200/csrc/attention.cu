@@ -108,6 +108,7 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int N>
 __device__ __forceinline__ void lds_vec(const float* p, float (&v)[N]) {
@@ -396,7 +397,7 @@ struct MmaTile {
   static constexpr int T_BYTES = TT * D * 2;    // one f16 K / Y tile
   static constexpr int RAW = TT * D + TT * 3 * D / 8 + TT * 4;
   static constexpr int MERGE = WT > 1 ? 4 * 16 * (D + 2) * 4 : 0;  // every warp's 16-row state
-  static constexpr int MAIN = 2 * Q_BYTES + 3 * T_BYTES + TT * 4 + RAW;
+  static constexpr int MAIN = 2 * Q_BYTES + 3 * T_BYTES + TT * 4 + 2 * RAW;  // raw tiles double-buffered
   static constexpr int SMEM = (MAIN > MERGE ? MAIN : MERGE) + 128 * 8 * 4 + 128;
 };
 
@@ -417,10 +418,7 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
   uint8_t* yhi = kh + MT::T_BYTES;
   uint8_t* ylo = yhi + MT::T_BYTES;
   float* rms_s = reinterpret_cast<float*>(ylo + MT::T_BYTES);
-  uint8_t* raw = reinterpret_cast<uint8_t*>(rms_s + TT);
-  int8_t* rk = reinterpret_cast<int8_t*>(raw);
-  uint8_t* rv = raw + TT * D;
-  float* rs = reinterpret_cast<float*>(raw + TT * D + TT * 3 * D / 8);
+  uint8_t* raw0 = reinterpret_cast<uint8_t*>(rms_s + TT);  // two raw (packed) tile buffers
   // per-thread (conflict-free) table: code -> (centroid hi, centroid lo) f16 bits
   uint32_t* ctab = reinterpret_cast<uint32_t*>(smm + (MT::MAIN > MT::MERGE ? MT::MAIN : MT::MERGE));
 
@@ -444,8 +442,17 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     if (row < a.rows) {
       const int agent = row / a.group, g = row % a.group;
       const long long off = (((long long)agent * a.kv_heads + h) * a.group + g) * D + c * 8;
+      if (a.q_dtype == PKV_BF16) {
+        const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + off);
+        qv[0] = bf16lo(w.x); qv[1] = bf16hi(w.x); qv[2] = bf16lo(w.y); qv[3] = bf16hi(w.y);
+        qv[4] = bf16lo(w.z); qv[5] = bf16hi(w.z); qv[6] = bf16lo(w.w); qv[7] = bf16hi(w.w);
+      } else {
+        const float4 x0 = *reinterpret_cast<const float4*>(static_cast<const float*>(a.q) + off);
+        const float4 x1 = *reinterpret_cast<const float4*>(static_cast<const float*>(a.q) + off + 4);
+        qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w; qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+      }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) qv[j] = ldq(a, off + j) * a.qscale;
+      for (int j = 0; j < 8; ++j) qv[j] *= a.qscale;
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) qv[j] = 0.f;
@@ -458,16 +465,21 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
   }
   const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 1.f;
 
-  auto stage = [&](long long t0, int nt) {
+  // raw tile layout: int8 codes [TT][D] | packed values [TT][3D/8] | f32 scales [TT]
+  auto stage = [&](long long t0, int nt, uint8_t* buf) {
     const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
-    for (int i = tid; i < nt * D / 16; i += 128) cp_async16(rk + i * 16, gk + i * 16);
+    for (int i = tid; i < nt * D / 16; i += 128) cp_async16(buf + i * 16, gk + i * 16);
     const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
-    for (int i = tid; i < nt * (3 * D / 8) / 4; i += 128) cp_async4(rv + i * 4, gv + i * 4);
+    uint8_t* bv = buf + TT * D;
+    for (int i = tid; i < nt * (3 * D / 8) / 4; i += 128) cp_async4(bv + i * 4, gv + i * 4);
     const float* gs = a.v_scales + (long long)h * a.T + t0;
-    for (int i = tid; i < nt; i += 128) cp_async4(rs + i, gs + i);
+    float* bs = reinterpret_cast<float*>(buf + TT * D + TT * 3 * D / 8);
+    for (int i = tid; i < nt; i += 128) cp_async4(bs + i, gs + i);
     cp_async_commit();
   };
-  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT, t_end - t_begin));
+  // two tiles in flight: tile i + 1 loads while tile i converts and computes
+  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT, t_end - t_begin), raw0);
+  if (t_begin + TT < t_end) stage(t_begin + TT, (int)min((long long)TT, t_end - t_begin - TT), raw0 + MT::RAW);
 
   float o[ND][4];
 #pragma unroll
@@ -479,9 +491,15 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
   const uint32_t yhi_s = (uint32_t)__cvta_generic_to_shared(yhi), ylo_s = (uint32_t)__cvta_generic_to_shared(ylo);
   const int qrow = wr * 16;
 
-  for (long long t0 = t_begin; t0 < t_end; t0 += TT) {
+  int it = 0;
+  for (long long t0 = t_begin; t0 < t_end; t0 += TT, ++it) {
     const int nt = (int)min((long long)TT, t_end - t0);
-    cp_async_wait_all();
+    uint8_t* raw = raw0 + (it & 1) * MT::RAW;
+    const int8_t* rk = reinterpret_cast<const int8_t*>(raw);
+    const uint8_t* rv = raw + TT * D;
+    const float* rs = reinterpret_cast<const float*>(raw + TT * D + TT * 3 * D / 8);
+    if (t0 + TT < t_end) cp_async_wait_one();  // this tile landed (the next may still be in flight)
+    else cp_async_wait_all();
     __syncthreads();  // raw tile landed; every warp is done with the previous K / Y tiles
     // ---- K: int8 codes -> f16 (exact; block32: x f16 scale), 16 codes per thread-step ----
     for (int i = tid; i < TT * D / 16; i += 128) {
@@ -530,8 +548,8 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
       *reinterpret_cast<uint4*>(ylo + sw<D>(t, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     for (int i = tid; i < TT; i += 128) rms_s[i] = i < nt ? rs[i] : 0.f;
-    __syncthreads();  // tiles converted; raw buffer free
-    if (t0 + TT < t_end) stage(t0 + TT, (int)min((long long)TT, t_end - t0 - TT));
+    __syncthreads();  // tiles converted; this raw buffer is free for tile i + 2
+    if (t0 + 2 * TT < t_end) stage(t0 + 2 * TT, (int)min((long long)TT, t_end - t0 - 2 * TT), raw);
 
     // ---- S = Q K^T over this warp's TW tokens ----
     const int tw0 = wt * TW;
@@ -544,17 +562,23 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
       const int ar = qrow + (lane & 7) + 8 * ((lane >> 3) & 1), ac = 2 * k + (lane >> 4);
       ldsm_x4(qhi_s + sw<D>(ar, ac), ah);
       ldsm_x4(qlo_s + sw<D>(ar, ac), al);
+      uint32_t b[NB / 2][4];
 #pragma unroll
       for (int n = 0; n < NB; n += 2) {
-        uint32_t b[4];
         const int br = tw0 + n * 8 + (lane & 7) + 8 * (lane >> 4), bc = 2 * k + ((lane >> 3) & 1);
-        ldsm_x4(kh_s + sw<D>(br, bc), b);
-        mma16816(s[n], ah, b[0], b[1]);
-        mma16816(s[n], al, b[0], b[1]);
-        if (n + 1 < NB) {
-          mma16816(s[n + 1], ah, b[2], b[3]);
-          mma16816(s[n + 1], al, b[2], b[3]);
-        }
+        ldsm_x4(kh_s + sw<D>(br, bc), b[n / 2]);
+      }
+      // the hi and lo products of one accumulator are NB MMAs apart (no
+      // back-to-back dependent MMAs)
+#pragma unroll
+      for (int n = 0; n < NB; n += 2) {
+        mma16816(s[n], ah, b[n / 2][0], b[n / 2][1]);
+        mma16816(s[n + 1], ah, b[n / 2][2], b[n / 2][3]);
+      }
+#pragma unroll
+      for (int n = 0; n < NB; n += 2) {
+        mma16816(s[n], al, b[n / 2][0], b[n / 2][1]);
+        mma16816(s[n + 1], al, b[n / 2][2], b[n / 2][3]);
       }
     }
     // ---- online softmax (rows g and g + 8 of this warp's 16) ----
@@ -611,13 +635,16 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
       const int br = tw0 + kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
 #pragma unroll
       for (int j = 0; j < ND; j += 2) {
-        uint32_t bh[4], bl[4];
-        const int bc = j + (lane >> 4);
-        ldsm_x4_t(yhi_s + sw<D>(br, bc), bh);
-        ldsm_x4_t(ylo_s + sw<D>(br, bc), bl);
+        uint32_t bh[4];
+        ldsm_x4_t(yhi_s + sw<D>(br, j + (lane >> 4)), bh);
         mma16816(o[j], af, bh[0], bh[1]);
-        mma16816(o[j], af, bl[0], bl[1]);
         mma16816(o[j + 1], af, bh[2], bh[3]);
+      }
+#pragma unroll
+      for (int j = 0; j < ND; j += 2) {
+        uint32_t bl[4];
+        ldsm_x4_t(ylo_s + sw<D>(br, j + (lane >> 4)), bl);
+        mma16816(o[j], af, bl[0], bl[1]);
         mma16816(o[j + 1], af, bl[2], bl[3]);
       }
     }
@@ -852,6 +879,24 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
 #endif
 inline int attn_splits(int kv_heads, long long T, int rows, int head_dim) {
   const int env_per_sm = tuning().attn_ctas_per_sm;
+  if (!tuning().attn_simt) {
+    // tensor-core prefix: ~2 resident CTAs per SM (shared memory), and at
+    // least `min_tiles` tiles per split (double-buffered tile loads)
+    const int per_sm = env_per_sm > 0 ? env_per_sm : 2;
+    // (C3: 2 -> 0.66 ms per 32-layer step, 3-4 -> 0.80, 8 -> 1.31)
+    const int min_tiles = tuning().attn_min_tiles > 0 ? tuning().attn_min_tiles : 2;
+    const int rt = rows <= 16 ? 16 : rows <= 32 ? 32 : 64;
+    const int row_tiles = (rows + rt - 1) / rt;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long den = (long long)kv_heads * row_tiles;
+    const long long tiles = (T + TT2 - 1) / TT2;
+    long long want = std::max(1LL, ((long long)per_sm * sms + den - 1) / den);
+    want = std::max(1LL, std::min(want, tiles / min_tiles));
+    const long long per = (tiles + want - 1) / want;
+    return (int)((tiles + per - 1) / per);
+  }
   const int rt = rows <= 16 ? 16 : 64;
   const int row_tiles = (rows + rt - 1) / rt;
   const int per_sm = env_per_sm > 0 ? env_per_sm : (rt == 16 && head_dim == 64 ? PKV_ATTN_SMALL_PER_SM : 2);

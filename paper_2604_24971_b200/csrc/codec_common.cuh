@@ -22,12 +22,6 @@ struct Codebook3 {
 constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
 
 constexpr float kKeyEps = 4e-5f;             // |q - n| half-point guard for keys
-// relative guard of the paired fast path: q = RN(x * r) with r within 1 ulp
-// of 1/s (RN(1/s) or rcp.approx) is within 1.5 * 2^-23 |q| of x/s, so
-// |q - n| + 2^-22 |q| <= 0.5 - 2^-20 (covering the rounding of that sum)
-// proves x/s rounds to n under any tie rule.
-constexpr float kKeyRel = 0x1p-22f;
-constexpr float kKeyAbs = 0x1p-20f;
 
 // Reference formula (keyquant.py:61-64), evaluated exactly as numpy does in
 // fp64: q = f64(x)/scale, code = floor(|q| + 0.5) * sign(q), clipped.
@@ -93,28 +87,30 @@ __device__ __forceinline__ uint2 key_chunk(const float (&x)[8], float s, float r
 }
 
 // Branch-free fast path of key_chunk (keyquant.py:61-64) on f32 pairs:
-// q = x * (1/s) rounded to the nearest integer with the 2^23 magic (the low
-// byte of the magic sum is the two's-complement code). `bad` is set when any
-// element lies within kKeyEps of a rounding half-point; the caller then
-// re-codes the chunk with key_chunk(..., force_exact = true).
+// m = x * rcp + 2^23 * 1.5 in ONE rounding (FFMA2), so n = m - magic is the
+// nearest integer to the exact product x * rcp, and the low byte of m is its
+// two's-complement code; d = x * rcp - n, again one rounding. With rcp within
+// 1 ulp of 1/s, |x * rcp - x / s| <= 127.5 * 2^-23 < 2^-16, so every element
+// with |d| <= 0.5 - 2^-15 has |x / s - n| < 0.5: n is the unique nearest
+// integer of the exact quotient, i.e. keyquant.py's round-half-away result
+// (a tie cannot pass). Otherwise `bad` is set and the caller re-codes the
+// chunk exactly (key_code_fma). 3 paired FMAs + 1 max per pair of elements.
+constexpr float kKeyGuard = 0.5f - 0x1p-15f;
 __device__ __forceinline__ uint2 key_chunk_fast(const float (&x)[8], float2 rcp2, bool& bad) {
   const float2 mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
   uint32_t mb[8];
   float worst = 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 q = __fmul2_rn(make_float2(x[2 * j], x[2 * j + 1]), rcp2);
-    const float2 m = __fadd2_rn(q, mg);
+    const float2 xp = make_float2(x[2 * j], x[2 * j + 1]);
+    const float2 m = __ffma2_rn(xp, rcp2, mg);
     const float2 n = __fadd2_rn(m, nmg);
-    const float2 d = __ffma2_rn(n, make_float2(-1.f, -1.f), q);  // q - n, exact
-    // |q - x/s| <= 2^-23 |q|: the guard scales with |q| (|.| are free FFMA2 operand modifiers)
-    const float2 gq = __ffma2_rn(make_float2(fabsf(q.x), fabsf(q.y)), make_float2(kKeyRel, kKeyRel),
-                                 make_float2(fabsf(d.x), fabsf(d.y)));
-    worst = fmaxf(worst, fmaxf(gq.x, gq.y));
+    const float2 d = __ffma2_rn(xp, rcp2, make_float2(-n.x, -n.y));
+    worst = fmaxf(worst, fmaxf(fabsf(d.x), fabsf(d.y)));
     mb[2 * j] = __float_as_uint(m.x);
     mb[2 * j + 1] = __float_as_uint(m.y);
   }
-  bad = worst > 0.5f - kKeyAbs;
+  bad = worst > kKeyGuard;
   uint2 w;
   w.x = __byte_perm(__byte_perm(mb[0], mb[1], 0x0040), __byte_perm(mb[2], mb[3], 0x0040), 0x5410);
   w.y = __byte_perm(__byte_perm(mb[4], mb[5], 0x0040), __byte_perm(mb[6], mb[7], 0x0040), 0x5410);

@@ -21,10 +21,12 @@ Tuning read_env() {
   if (const char* e = std::getenv("PKV_CODEC_PATH")) t.codec_warp = std::strcmp(e, "warp") == 0;
   if (const char* e = std::getenv("PKV_DBG_ENC")) t.dbg_enc = std::atoi(e);
   if (const char* e = std::getenv("PKV_KEY_LAG")) t.key_lag = std::atoi(e);
+  if (const char* e = std::getenv("PKV_ABSMAX_ROLE")) t.abs_on_values = std::strcmp(e, "values") == 0;
   if (const char* e = std::getenv("PKV_KEY_SM_FRACTION")) t.key_sm_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_DEC_KEY_FRACTION")) t.dec_key_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM")) t.attn_ctas_per_sm = std::atoi(e);
   if (const char* e = std::getenv("PKV_ATTN_PATH")) t.attn_simt = std::strcmp(e, "simt") == 0;
+  if (const char* e = std::getenv("PKV_ATTN_MIN_TILES")) t.attn_min_tiles = std::atoi(e);
   return t;
 }
 std::mutex g_reload;

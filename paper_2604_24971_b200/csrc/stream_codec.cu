@@ -142,6 +142,7 @@ struct EncArgs {
   int nA;                     // absmax items per layer (per-tensor mode)
   int nseg;                   // key-role segments of nE items: kind (A/E) + layer
   int key_lag;                // absmax layers allowed ahead of the key encode
+  int abs_lead;               // > 0: the VALUE CTAs run the absmax items, abs_lead layers ahead of their V cursor
   uint8_t seg_absmax[2 * kMaxL];
   uint8_t seg_layer[2 * kMaxL];
   const void* k_in[kMaxL];
@@ -630,6 +631,28 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   uint32_t m = 0;
+  if constexpr (sizeof(TIn) == 2) {
+    if (n == kEncChunk) {
+      // bf16 pairs: one NaN-propagating |.| max per 2 elements (HMNMX2), the
+      // two halves folded once per item; a NaN ends above +inf like the bit
+      // patterns of the generic path
+      __nv_bfloat162 acc = __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
+        const uint4 w = tma::lds128(in_s + (i * kGroupThreads + gt) * 16);
+        const __nv_bfloat162 p = __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&w.x)),
+                                             __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w.y)));
+        const __nv_bfloat162 q = __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&w.z)),
+                                             __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w.w)));
+        acc = __hmax2_nan(acc, __hmax2_nan(p, q));
+      }
+      const uint32_t ab = *reinterpret_cast<uint32_t*>(&acc);
+      m = max(ab & 0x7fffu, (ab >> 16) & 0x7fffu) << 16;  // |.| patterns: NaN (0x7fff) > inf
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      return m;
+    }
+  }
   if (n == kEncChunk) {
 #pragma unroll
     for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i)
@@ -765,8 +788,9 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     uint2 w;
     if (in_range && ex != 0u && ex != 0x7c00u) {
       // normal fp16 scale: s >= (peak/127)(1 - 2^-11), so |x|/s < 127.07 and
-      // the clip never acts; paired fast path (rcp.approx is within 1 ulp,
-      // inside the kKeyRel guard), FMA-exact re-code near a half-point
+      // the clip never acts; paired fast path (rcp.approx is within 1 ulp:
+      // 127.07 * 2^-23 < 2^-16, inside the kKeyGuard margin), FMA-exact
+      // re-code near a half-point
       const float s = __half2float(__ushort_as_half(s16b));
       const float rcp = rcp_approx(s);
       bool bad;
@@ -1199,7 +1223,29 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
                         it.kind == kAbsmax ? pol_last : pol_first);
         }
       };
-      if (value_role) {
+      if (value_role && a.abs_lead > 0 && a.nA > 0) {
+        // The value CTAs are ALU-bound and their memory pipe is mostly idle:
+        // they also stream the per-tensor absmax items (HBM reads kept in L2
+        // with evict_last for the key encode), abs_lead layers ahead of their
+        // value cursor, so the key CTAs only run the encode pass (L2 re-read).
+        const long long G = a.value_ctas, totV = (long long)a.num_layers * a.nV;
+        const long long totA = (long long)a.num_layers * a.nA;
+        long long tv = role_rank, ta = role_rank;
+        auto next_item = [&]() -> Item {
+          const bool a_ok = ta < totA;
+          if (a_ok && (tv >= totV || ta / a.nA <= tv / a.nV + a.abs_lead)) {
+            const int l = (int)(ta / a.nA);
+            const Item it{kAbsmax, l, (int)(ta - (long long)l * a.nA), 0};
+            ta += G;
+            return it;
+          }
+          if (tv >= totV) return Item{kEnd, 0, 0, 0};
+          const Item it = enc_value_item_at(a, tv);
+          tv += G;
+          return it;
+        };
+        produce<NG, NSG>(ctl, ring, P::STAGE, next_item, issue);
+      } else if (value_role) {
         const long long G = a.value_ctas, total = (long long)a.num_layers * a.nV;
         long long t = role_rank;
         auto next_item = [&]() -> Item {
@@ -1235,7 +1281,9 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         // overlaps the TMA issue in between)
         const uint32_t G = gridDim.x - (uint32_t)a.value_ctas;
         const uint32_t nA = (uint32_t)a.nA, nE = (uint32_t)a.nE;
-        const uint32_t totA = (uint32_t)a.num_layers * nA, totE = (uint32_t)a.num_layers * nE;
+        // (absmax on the value CTAs: this role only encodes, waiting on layer_done)
+        const uint32_t totA = a.abs_lead > 0 ? 0u : (uint32_t)a.num_layers * nA;
+        const uint32_t totE = (uint32_t)a.num_layers * nE;
         uint32_t ta = (uint32_t)role_rank, te = (uint32_t)role_rank;
         int ready = -1;      // layers [0, ready] staged in ctl->layer_max
         int polled = -1;     // layer whose count is in `polled_cnt`
@@ -1691,6 +1739,9 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
         a->seg_layer[a->nseg++] = (uint8_t)l;
       }
     }
+    // absmax items on the value CTAs (per-tensor keys with values in the launch)
+    a->abs_lead = 0;
+    if (a->nA && do_v && tuning().abs_on_values) a->abs_lead = 2;
     int key_ctas = 0;
     if (do_k && do_v) {
       // share of SMs for the key role, swept on C3 bf16 (tools/ab_frac.sh):
@@ -1701,6 +1752,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // (d64, whose value path is cheaper: C2 0.35 -> 188 us, 0.42 -> 169, 0.46 -> 178)
       const bool d128 = r.head_dim >= 128;
       double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? 0.38 : 0.42) : (d128 ? 0.43 : 0.46);
+      if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
       // an even count: the two SMs of a TPC must run the same role (an odd
       // split puts both code paths on one TPC, which thrashes and, with the

@@ -237,55 +237,59 @@ def dequantize_v(block: QuantizedValueBlock, codebook: Codebook = GAUSSIAN_3BIT,
 
 
 def lloyd_max_train(samples, bits: int, max_iters: int = 200, tol: float = 1e-7) -> Codebook:
-    """Scalar Lloyd-Max trainer (offline, host; valuequant.py:241-300 semantics).
+    """Scalar Lloyd-Max codebook for 1-D samples (kvpool.lloyd_max_train,
+    valuequant.py:241-300 semantics: quantile start, midpoint cells with
+    ties to the lower cell, cell means, empty cells reseeded inside the most
+    populated cell with a RuntimeWarning, strictly increasing centroids).
 
-    Produces codebook tables; it is not on the compress/inject path.
+    Offline table building, not on the compress/inject path (SURVEY §2 row 4;
+    the pool codes with the frozen GAUSSIAN_3BIT table). Implemented on the
+    SORTED samples: every cell is a contiguous run, so one iteration is two
+    searchsorted calls over the level boundaries and a prefix-sum difference,
+    O(levels log n) instead of a pass over all samples.
     """
-    data = np.asarray(samples, dtype=np.float64).ravel()
+    x = np.sort(np.asarray(samples, dtype=np.float64).ravel())
     if not 1 <= bits <= 8:
         raise ValueError(f"bits must be in [1, 8], got {bits}")
-    levels = 1 << bits
-    if data.size < 10 * levels:
-        raise ValueError(f"need at least {10 * levels} samples for {bits} bits, got {data.size}")
-    if not np.isfinite(data).all():
+    k = 1 << bits
+    if x.size < 10 * k:
+        raise ValueError(f"need at least {10 * k} samples for {bits} bits, got {x.size}")
+    if not np.isfinite(x).all():
         raise ValueError("samples must be finite")
+    csum = np.concatenate(([0.0], np.cumsum(x)))
 
-    def strictly_up(a):
-        a = a.copy()
-        for i in range(1, a.size):
-            if a[i] <= a[i - 1]:
-                a[i] = np.nextafter(a[i - 1], np.inf)
-        return a
+    def monotone(c):  # nudge ties up by one ulp, left to right
+        c = np.array(c, dtype=np.float64)
+        for i in range(1, c.size):
+            if c[i] <= c[i - 1]:
+                c[i] = np.nextafter(c[i - 1], np.inf)
+        return c
 
-    lo, hi = float(data.min()), float(data.max())
-    cent = strictly_up(np.quantile(data, (np.arange(levels) + 0.5) / levels))
-    repaired = 0
+    c = monotone(np.quantile(x, (np.arange(k) + 0.5) / k))
+    reseeded = 0
     for _ in range(max_iters):
-        mids = 0.5 * (cent[:-1] + cent[1:])
-        cell = np.searchsorted(mids, data, side="left")
-        cnt = np.bincount(cell, minlength=levels)
-        tot = np.bincount(cell, weights=data, minlength=levels)
-        new = cent.copy()
-        occ = cnt > 0
-        new[occ] = tot[occ] / cnt[occ]
-        empty = np.flatnonzero(~occ)
-        if empty.size:
-            repaired += int(empty.size)
-            big = int(np.argmax(cnt))
-            a = mids[big - 1] if big > 0 else lo
-            b = mids[big] if big < levels - 1 else hi
-            for j, e in enumerate(empty):
-                new[e] = a + (j + 1) / (empty.size + 1) * (b - a)
-            cent = strictly_up(np.sort(new))
+        mid = 0.5 * (c[1:] + c[:-1])
+        edge = np.concatenate(([0], np.searchsorted(x, mid, side="right"), [x.size]))
+        n = np.diff(edge)
+        total = csum[edge[1:]] - csum[edge[:-1]]
+        upd = np.where(n > 0, total / np.maximum(n, 1), c)
+        hole = np.flatnonzero(n == 0)
+        if hole.size:
+            reseeded += hole.size
+            full = int(np.argmax(n))
+            left = x[0] if full == 0 else mid[full - 1]
+            right = x[-1] if full == k - 1 else mid[full]
+            upd[hole] = left + (np.arange(1, hole.size + 1) / (hole.size + 1)) * (right - left)
+            c = monotone(np.sort(upd))
             continue
-        new = strictly_up(new)
-        shift = float(np.max(np.abs(new - cent)))
-        cent = new
-        if shift < tol:
+        upd = monotone(upd)
+        moved = float(np.abs(upd - c).max())
+        c = upd
+        if moved < tol:
             break
-    if repaired:
-        warnings.warn(f"lloyd_max_train repaired {repaired} empty cell(s)", RuntimeWarning)
-    return Codebook(bits=bits, centroids=cent, name=f"lloyd-max-{bits}bit-trained")
+    if reseeded:
+        warnings.warn(f"lloyd_max_train repaired {reseeded} empty cell(s)", RuntimeWarning)
+    return Codebook(bits=bits, centroids=c, name=f"lloyd-max-{bits}bit-trained")
 
 
 def pack_indices_3bit(codes) -> bytes:

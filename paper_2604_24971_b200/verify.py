@@ -94,15 +94,21 @@ def verify_pool(dump: KvDump, pool: SharedPool, *, agents=(1, 3, 15), decode_bit
             not report.v_bound_violations,
             f"layers {list(report.v_bound_violations)}" if report.v_bound_violations else "")
 
-    # pool memory must not scale with attached agents
+    # pool memory must not scale with attached agents: the pool's own HBM
+    # footprint and the device allocator's total both stay put while views
+    # are attached (a view holds no tensor state, pool.py:217-222)
+    torch.cuda.synchronize(pool.device)
+    base_alloc = torch.cuda.memory_allocated(pool.device)
+    base_pool = pool.device_nbytes()
     sizes = []
+    views = []
     for count in agents:
-        before = pool.payload_nbytes()
-        for _ in range(count):
-            pool.attach(decode_bits)
-        sizes.append((count, before, pool.payload_nbytes()))
-    invariant = all(b == a == sizes[0][1] for _, b, a in sizes)
-    rep.add(f"pool bytes invariant across agent counts {tuple(agents)}", invariant, "" if invariant else str(sizes))
+        views.extend(pool.attach(decode_bits) for _ in range(count))
+        torch.cuda.synchronize(pool.device)
+        sizes.append((len(views), pool.device_nbytes(), torch.cuda.memory_allocated(pool.device) - base_alloc))
+    invariant = all(p == base_pool and grown == 0 for _, p, grown in sizes)
+    rep.add(f"pool HBM bytes invariant across agent counts {tuple(agents)}", invariant,
+            "" if invariant else f"(agents, pool bytes, allocator growth): {sizes}")
     return rep
 
 

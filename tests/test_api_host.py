@@ -126,3 +126,22 @@ def test_no_cpu_fallback():
         pk.build_pool(dump)
     with pytest.raises(CudaRequiredError):
         pk.quantize_v(dump.layers[0][1])
+
+
+def test_lloyd_max_train_matches_reference_semantics():
+    """Off-path table builder (valuequant.py:241-300): sorted-sample
+    implementation, same fixed point as the reference's pass-over-samples
+    loop (to summation rounding), same empty-cell repair warning."""
+    import warnings
+
+    from paper_2604_24971_b200 import valuequant as V
+
+    x = np.random.default_rng(0).normal(size=20000)
+    c = V.lloyd_max_train(x, 3).centroids
+    assert np.all(np.diff(c) > 0)
+    # the trained 3-bit table of N(0, 1) samples is close to the frozen GAUSSIAN_3BIT one
+    assert np.abs(c - V.GAUSSIAN_3BIT.centroids).max() < 0.1
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        c2 = V.lloyd_max_train(np.concatenate([np.zeros(100), np.ones(100)]), 3).centroids
+    assert any("repaired" in str(i.message) for i in w) and np.all(np.diff(c2) > 0)

@@ -105,6 +105,7 @@ def test_streamed_decode_matches_materialized_decode(tiny_llama, agents):
     B = agents
     full = ids.expand(B, -1)
     # reference: materialised 32-bit cache, sdpa, manual greedy loop
+    pool_bytes = pool.device_nbytes()
     ref_cache = hf.build_cache(pool.attach(32), "materialize", batch=B, dtype=torch.float32)
     st_cache = hf.build_cache(pool.attach(32), "stream", batch=B)
     tiny_llama.set_attn_implementation("sdpa")
@@ -130,11 +131,17 @@ def test_streamed_decode_matches_materialized_decode(tiny_llama, agents):
     tiny_llama.set_attn_implementation("sdpa")
     for r, s in zip(ref_logits, st_logits):
         rel = float((r - s).abs().max() / r.abs().max())
-        assert rel < 2e-2, rel
+        assert rel < 5e-3, rel
         assert torch.equal(r.argmax(-1), s.argmax(-1))
     assert st_cache.get_seq_length() == 32 + 8 + steps - 1
-    # pool memory is shared: streaming agents add only their tails
-    assert pool.payload_nbytes() == pool.payload_nbytes()
+    # pool memory is shared: the pool's HBM footprint did not change, and the
+    # streaming agents hold only their private tails (no per-agent prefix copy)
+    assert pool.device_nbytes() == pool_bytes
+
+    # every streamed layer holds only its [B, H, capacity, D] bf16 tail buffers
+    for layer in st_cache.layers:
+        assert layer.keys.shape[2] == layer.capacity and layer.values.shape == layer.keys.shape
+        assert layer.keys.dtype == torch.bfloat16 and layer.tail_len == 8 + steps - 1
 
 
 def test_greedy_continuation_modes_agree(tiny_llama):
@@ -148,6 +155,6 @@ def test_greedy_continuation_modes_agree(tiny_llama):
     b = hf.greedy_continuation(tiny_llama, ids, pool.attach(32), 5, mode="stream", batch=2)
     tiny_llama.set_attn_implementation("sdpa")
     assert a.shape == (2, 5)
-    assert (a == b).float().mean() >= 0.8
+    # 32-bit decode: the streamed pool attention must pick the same tokens
+    assert torch.equal(a, b), (a, b)
     assert torch.equal(a[0], a[1]) and torch.equal(b[0], b[1])
-    _ = np  # noqa: F841
