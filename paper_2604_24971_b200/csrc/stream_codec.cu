@@ -1750,8 +1750,10 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // smooth: SMs sharing instruction caches should run one role, so
       // where the role boundary falls matters. PKV_KEY_SM_FRACTION overrides
       // (d64, whose value path is cheaper: C2 0.35 -> 188 us, 0.42 -> 169, 0.46 -> 178)
+      // (round 2, after the key fast-path change: C3 bf16 0.34 -> 253 us, 0.38 -> 261,
+      // 0.42 -> 275; C3 f32 0.38 -> 365 us, 0.42 -> 335, 0.45 -> 327, 0.49 -> 350)
       const bool d128 = r.head_dim >= 128;
-      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? 0.38 : 0.42) : (d128 ? 0.43 : 0.46);
+      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.45 : 0.34) : 0.42) : (d128 ? 0.43 : 0.46);
       if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
       // an even count: the two SMs of a TPC must run the same role (an odd

@@ -2,9 +2,10 @@
 head_dim 64/128, one B200.
 
 Each point: `build_pool` (pkv_encode, all layers) and a full materialise to
-bf16 (pkv_decode), CUDA-graph captured, inputs generated on the device
-(torch generator). Prints one JSON line per point; GB/s use the §8(d)
+bf16 (pkv_decode), CUDA-graph captured, inputs (f32 or bf16) generated on the
+device (torch generator). Prints one JSON line per point; GB/s use the §8(d)
 algorithmic bytes. Layers are reduced at long contexts to bound memory.
+Bit-exactness along the sweep: tests/test_gpu_sweep_parity.py.
 """
 
 from __future__ import annotations
@@ -33,13 +34,15 @@ def algorithmic_bytes(L, H, D, T, in_b=2, out_b=2):
     return comp, deq
 
 
-def point(D, T, max_bytes=24e9, reps=10):
+def point(D, T, dtype="bf16", max_bytes=24e9, reps=10):
     L, H = SHAPES[D]
-    per_layer = 2 * H * T * D * 2 * 2  # inputs + outputs, bf16
+    in_b = 2 if dtype == "bf16" else 4
+    per_layer = 2 * H * T * D * (in_b + 2)  # inputs + outputs
     L = max(1, min(L, int(max_bytes // per_layer)))
     g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
     dev = torch.device("cuda")
-    dump = pk.synth_gaussian_dump(g, seed=0, device=dev, dtype=torch.bfloat16, generator="torch")
+    dump = pk.synth_gaussian_dump(g, seed=0, device=dev, dtype=torch.bfloat16 if in_b == 2 else torch.float32,
+                                  generator="torch")
     ks, vs = [k for k, _ in dump.layers], [v for _, v in dump.layers]
     arena = _Arena(g, L, "tensor", dev)
     kb, vb, _ = _encode_layers(ks, vs, g, pk.GAUSSIAN_3BIT, None, "tensor", device=dev, arena=arena)
@@ -80,10 +83,11 @@ def point(D, T, max_bytes=24e9, reps=10):
         return a.elapsed_time(b) / reps
 
     te, td = timeit(graph(enc)), timeit(graph(dec))
-    cb, dbb = algorithmic_bytes(L, H, D, T)
+    cb, dbb = algorithmic_bytes(L, H, D, T, in_b=in_b)
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6561.0) \
         if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6561.0
-    res = {"head_dim": D, "seq_len": T, "layers": L, "kv_heads": H, "encode_ms": te, "decode_ms": td,
+    res = {"head_dim": D, "seq_len": T, "layers": L, "kv_heads": H, "dtype_in": dtype, "encode_ms": te,
+           "decode_ms": td, "encode_frac_of_hbm_peak": cb / te / 1e6 / peak,
            "encode_gbs": cb / te / 1e6, "decode_gbs": dbb / td / 1e6,
            "step_gbs": (cb + dbb) / (te + td) / 1e6, "frac_of_hbm_peak": (cb + dbb) / (te + td) / 1e6 / peak}
     del dump, ks, vs, arena, pool, ko, vo
@@ -95,7 +99,9 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", default="1024,2048,4096,8192,16384,32768,65536,131072")
     ap.add_argument("--dims", default="64,128")
+    ap.add_argument("--dtypes", default="f32,bf16")
     a = ap.parse_args()
-    for D in (int(x) for x in a.dims.split(",")):
-        for T in (int(x) for x in a.tokens.split(",")):
-            print(json.dumps(point(D, T)), flush=True)
+    for dt in a.dtypes.split(","):
+        for D in (int(x) for x in a.dims.split(",")):
+            for T in (int(x) for x in a.tokens.split(",")):
+                print(json.dumps(point(D, T, dt)), flush=True)
