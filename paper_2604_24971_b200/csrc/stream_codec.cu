@@ -43,7 +43,17 @@ constexpr int kEncGroups = 3;
 #ifndef PKV_ENC_CHUNK
 #define PKV_ENC_CHUNK 16384
 #endif
-constexpr int kEncChunk = PKV_ENC_CHUNK;  // elements per encode work item
+#ifndef PKV_ENC_CHUNK_F32
+#define PKV_ENC_CHUNK_F32 8192
+#endif
+// elements per encode work item: 32 KB stages for both input types (two
+// stages per consumer group), so f32 key items can also be copied to
+// registers and their stage released before the math
+template <typename TIn>
+constexpr int enc_chunk() {
+  return sizeof(TIn) == 4 ? PKV_ENC_CHUNK_F32 : PKV_ENC_CHUNK;
+}
+inline int enc_chunk_for(int elem_bytes) { return elem_bytes == 4 ? PKV_ENC_CHUNK_F32 : PKV_ENC_CHUNK; }
 #ifndef PKV_B32_UNROLL
 #define PKV_B32_UNROLL 2
 #endif
@@ -441,7 +451,7 @@ template <int D, typename TIn, bool SYM, bool SIGN>
 __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, int wig, int lane, double* R,
                                uint8_t* C) {
   using G = VL<D>;
-  using TL = Tile<D, (int)sizeof(TIn), kEncChunk>;
+  using TL = Tile<D, (int)sizeof(TIn), enc_chunk<TIn>()>;
   constexpr int NP = G::NP, NCL = G::NCL;
   const int r = lane % G::VPW, s = lane / G::VPW;
   const long long vbase = (long long)it.idx * TL::VR;
@@ -628,6 +638,7 @@ __device__ __forceinline__ uint32_t lds_absmax8<float>(uint32_t a) {
 
 template <typename TIn>
 __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt) {
+  constexpr int kEncChunk = enc_chunk<TIn>();
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   uint32_t m = 0;
@@ -675,6 +686,7 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
 template <typename TIn, class Release>
 __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane,
                              const uint32_t* layer_max, Release release, bool& released) {
+  constexpr int kEncChunk = enc_chunk<TIn>();
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
@@ -689,15 +701,20 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
     const float rcp = 1.0f / s;
     const bool exact_all = !(s >= 1e-30f);
     constexpr int ITERS = kEncChunk / 8 / kGroupThreads;
-    if constexpr (sizeof(TIn) == 2 && kKeyEarlyRelease) {
+    if constexpr (kKeyEarlyRelease) {
       if (n == kEncChunk && !exact_all) {
-        // bf16 full item: the lane's 16 chunks (64 registers) are copied out
-        // and the stage released at once, so its refill overlaps the math.
-        // Branch-free pass; chunks near a half-point are re-coded from global
-        // memory afterwards (rare; the stage may be refilled by then)
-        uint4 raw[ITERS];
+        // full item: the lane's ITERS chunks of 8 inputs (64 registers for
+        // both input types: 32 KB stages) are copied out and the stage
+        // released at once, so its refill overlaps the math. Branch-free
+        // pass; chunks near a half-point are re-coded from global memory
+        // afterwards (rare; the stage may be refilled by then)
+        constexpr int UPC = (int)sizeof(TIn) / 2;  // 16-byte units per chunk of 8 inputs
+        uint4 raw[ITERS * UPC];
 #pragma unroll
-        for (int i = 0; i < ITERS; ++i) raw[i] = tma::lds128(in_s + (i * kGroupThreads + gt) * 16);
+        for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+          for (int h = 0; h < UPC; ++h)
+            raw[i * UPC + h] = tma::lds128(in_s + ((i * kGroupThreads + gt) * UPC + h) * 16);
         release();
         released = true;
         uint32_t need = 0;
@@ -705,21 +722,28 @@ __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, in
         for (int i = 0; i < ITERS; ++i) {
           const int u = i * kGroupThreads + gt;
           float x[8];
-          x[0] = bf16lo(raw[i].x); x[1] = bf16hi(raw[i].x); x[2] = bf16lo(raw[i].y); x[3] = bf16hi(raw[i].y);
-          x[4] = bf16lo(raw[i].z); x[5] = bf16hi(raw[i].z); x[6] = bf16lo(raw[i].w); x[7] = bf16hi(raw[i].w);
+          if constexpr (UPC == 1) {
+            const uint4 r = raw[i];
+            x[0] = bf16lo(r.x); x[1] = bf16hi(r.x); x[2] = bf16lo(r.y); x[3] = bf16hi(r.y);
+            x[4] = bf16lo(r.z); x[5] = bf16hi(r.z); x[6] = bf16lo(r.w); x[7] = bf16hi(r.w);
+          } else {
+            const uint4 r0 = raw[2 * i], r1 = raw[2 * i + 1];
+            x[0] = __uint_as_float(r0.x); x[1] = __uint_as_float(r0.y); x[2] = __uint_as_float(r0.z);
+            x[3] = __uint_as_float(r0.w); x[4] = __uint_as_float(r1.x); x[5] = __uint_as_float(r1.y);
+            x[6] = __uint_as_float(r1.z); x[7] = __uint_as_float(r1.w);
+          }
           bool bad;
           st_u2(dst + u * 8, key_chunk_fast(x, make_float2(rcp, rcp), bad));
           need |= (uint32_t)bad << i;
         }
-        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const TIn*>(a.k_in[it.layer]) + e0);
+        const TIn* src = static_cast<const TIn*>(a.k_in[it.layer]) + e0;
 #pragma unroll 1
         while (need) {
           const int i = __ffs(need) - 1;
           need &= need - 1;
           const int u = i * kGroupThreads + gt;
-          const uint4 r = __ldg(src + u);
-          const float x[8] = {bf16lo(r.x), bf16hi(r.x), bf16lo(r.y), bf16hi(r.y),
-                              bf16lo(r.z), bf16hi(r.z), bf16lo(r.w), bf16hi(r.w)};
+          float x[8];
+          load8(src + u * 8, x);
           uint32_t c[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) c[j] = key_code_fma(x[j], s, rcp, -128, 127);
@@ -1051,7 +1075,7 @@ constexpr int kMaxSG = 4;
 template <int EB_IN>
 struct EncPlan {
   static constexpr int NG = kEncGroups;
-  static constexpr int STAGE = kEncChunk * EB_IN;
+  static constexpr int STAGE = (EB_IN == 4 ? PKV_ENC_CHUNK_F32 : PKV_ENC_CHUNK) * EB_IN;
   static constexpr int NSG = kEncRingBytes / STAGE / NG;  // stages per group
   static_assert(NSG >= 1 && NSG <= kMaxSG, "ring depth");
 };
@@ -1166,7 +1190,7 @@ __device__ __forceinline__ void produce(Ctl* ctl, uint8_t* ring, int stage_bytes
 template <int D, typename TIn, bool SYM, bool SIGN>
 __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_constant__ EncArgs a) {
   using P = EncPlan<(int)sizeof(TIn)>;
-  using TL = Tile<D, (int)sizeof(TIn), kEncChunk>;
+  using TL = Tile<D, (int)sizeof(TIn), enc_chunk<TIn>()>;
   constexpr int NG = P::NG, NSG = P::NSG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = align1024(smem_raw);
@@ -1216,6 +1240,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
                                 cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
         } else {
           // absmax reads keep the keys in L2 for the key-encode phase
+          constexpr int kEncChunk = enc_chunk<TIn>();
           const long long e0 = (long long)it.idx * kEncChunk;
           const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
           tma::mbar_arrive_expect_tx(bar, bytes);
@@ -1639,10 +1664,9 @@ bool a16(const void* p) { return p == nullptr || aligned(p, 16); }
 bool head_dim_streamable(int d) { return d == 16 || d == 32 || d == 64 || d == 128; }
 
 size_t workspace_bytes(int num_layers, long long num_vectors, int head_dim) {
-  const long long nelem = num_vectors * (long long)std::max(head_dim, 1);
-  const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
+  (void)num_vectors;
+  (void)head_dim;
   const long long L = std::min(std::max(num_layers, 0), kMaxL);
-  (void)kch;
   return (size_t)(L * 8 + 16);  // [u32 layer_max L][u32 layer_done L / key barrier]
 }
 
@@ -1668,6 +1692,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   std::memcpy(a->sign_bits, r.sign_bits, sizeof(a->sign_bits));
   a->status = r.status;
   a->replay_count = r.replay_count;
+  const int kEncChunk = enc_chunk_for(eb);
   const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
   const long long vr = kEncChunk / std::max(r.head_dim, 1);
   a->nE = do_k ? (int)kch : 0;
