@@ -22,6 +22,7 @@ Tuning read_env() {
   if (const char* e = std::getenv("PKV_DBG_ENC")) t.dbg_enc = std::atoi(e);
   if (const char* e = std::getenv("PKV_KEY_LAG")) t.key_lag = std::atoi(e);
   if (const char* e = std::getenv("PKV_ABSMAX_ROLE")) t.abs_on_values = std::strcmp(e, "values") == 0;
+  if (const char* e = std::getenv("PKV_ENC_ROLES")) t.enc_co = std::strcmp(e, "co") == 0;
   if (const char* e = std::getenv("PKV_KEY_SM_FRACTION")) t.key_sm_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_DEC_KEY_FRACTION")) t.dec_key_fraction = std::atof(e);
   if (const char* e = std::getenv("PKV_ATTN_CTAS_PER_SM")) t.attn_ctas_per_sm = std::atoi(e);

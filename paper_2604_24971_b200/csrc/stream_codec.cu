@@ -86,7 +86,7 @@ constexpr int dec_groups() {
   return sizeof(TOut) == 2 ? 3 : 2;
 }
 
-enum ItemKind : int { kEnd = 0, kAbsmax = 1, kKeyEnc = 2, kValEnc = 3, kKeyDec = 4, kValDec = 5, kBarrier = 6 };
+enum ItemKind : int { kEnd = 0, kAbsmax = 1, kKeyEnc = 2, kValEnc = 3, kKeyDec = 4, kValDec = 5, kBarrier = 6, kNone = 7 };
 
 struct Item {
   int kind;
@@ -113,16 +113,17 @@ struct VL {
 // Geometry of a head-vector tile of CHUNK elements (VR vectors of D) held as
 // TMA boxes of BR rows x IB bytes (IB = swizzle span), NCB boxes across a row
 // and NRB boxes down.
-template <int D, int EB, int CHUNK>
+template <int D, int EB, int CHUNK, int WPG = kWarpsPerGroup>
 struct Tile {
   static constexpr int RB = D * EB;               // bytes per head vector
   static constexpr int IB = RB < 128 ? RB : 128;  // inner box bytes
   static constexpr int NCB = RB / IB;
   static constexpr int VR = CHUNK / D;            // vectors per item
-  static constexpr int BR = VR < 256 ? VR : 256;  // rows per box
-  static constexpr int NRB = VR / BR;
+  static constexpr int NRB = (VR + 255) / 256;    // boxes down (TMA box rows <= 256)
+  static constexpr int BR = VR / NRB;             // rows per box
+  static_assert(BR * NRB == VR, "item rows split into equal boxes");
   static constexpr int BOX_BYTES = BR * IB;
-  static constexpr int PER_PASS = kWarpsPerGroup * VL<D>::VPW;
+  static constexpr int PER_PASS = WPG * VL<D>::VPW;
   static constexpr int PASSES = VR / PER_PASS;
   static_assert(VR % PER_PASS == 0, "item must hold whole passes");
   // byte offset of 16-byte unit u of vector vr inside the tile
@@ -153,6 +154,7 @@ struct EncArgs {
   int nseg;                   // key-role segments of nE items: kind (A/E) + layer
   int key_lag;                // absmax layers allowed ahead of the key encode
   int abs_lead;               // > 0: the VALUE CTAs run the absmax items, abs_lead layers ahead of their V cursor
+  int co_roles;               // enc_co_kernel: 0 = values on groups 0-2 + keys on group 3, 1 = all values, 2 = all keys
   uint8_t seg_absmax[2 * kMaxL];
   uint8_t seg_layer[2 * kMaxL];
   const void* k_in[kMaxL];
@@ -447,11 +449,11 @@ __device__ __forceinline__ void stg_words(uint8_t* dst, const uint32_t (&w)[NW])
 // ---------------------------------------------------------------------------
 // encode: value item (VR head vectors)
 // ---------------------------------------------------------------------------
-template <int D, typename TIn, bool SYM, bool SIGN>
+template <int D, typename TIn, bool SYM, bool SIGN, int CH, int WPG>
 __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, int wig, int lane, double* R,
                                uint8_t* C) {
   using G = VL<D>;
-  using TL = Tile<D, (int)sizeof(TIn), enc_chunk<TIn>()>;
+  using TL = Tile<D, (int)sizeof(TIn), CH, WPG>;
   constexpr int NP = G::NP, NCL = G::NCL;
   const int r = lane % G::VPW, s = lane / G::VPW;
   const long long vbase = (long long)it.idx * TL::VR;
@@ -636,9 +638,9 @@ __device__ __forceinline__ uint32_t lds_absmax8<float>(uint32_t a) {
   return max(m, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu), max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
 }
 
-template <typename TIn>
+template <typename TIn, int CH, int GT>
 __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt) {
-  constexpr int kEncChunk = enc_chunk<TIn>();
+  constexpr int kEncChunk = CH, kGroupThreads = GT;
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   uint32_t m = 0;
@@ -683,10 +685,10 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
 // release() hands the input stage back to the producer; a path that has
 // copied the stage into registers calls it before computing (and the caller
 // then must not release again: `released` is set).
-template <typename TIn, class Release>
+template <typename TIn, int CH, int GT, class Release>
 __device__ void enc_key_item(const EncArgs& a, const Item& it, uint32_t in_s, int gt, int lane,
                              const uint32_t* layer_max, Release release, bool& released) {
-  constexpr int kEncChunk = enc_chunk<TIn>();
+  constexpr int kEncChunk = CH, kGroupThreads = GT;
   const long long e0 = (long long)it.idx * kEncChunk;
   const int n = (int)min((long long)kEncChunk, a.nelem - e0);
   int8_t* dst = a.k_codes[it.layer] + e0;
@@ -1069,7 +1071,7 @@ __device__ __forceinline__ Item dec_item(const DecArgs& a, unsigned int t) {
 // (a layer-max wait, an fp64 replay) only ever stalls its own group. Encode
 // outputs are small and go straight to global memory; decode outputs are
 // staged in two buffers per group and written back by TMA stores.
-constexpr int kMaxGroups = 3;
+constexpr int kMaxGroups = 4;
 constexpr int kMaxSG = 4;
 
 template <int EB_IN>
@@ -1394,7 +1396,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);
     };
     if (it.kind == kAbsmax) {
-      const uint32_t m = skip ? 0u : enc_absmax_item<TIn>(a, it, in_s, gt);
+      const uint32_t m = skip ? 0u : enc_absmax_item<TIn, enc_chunk<TIn>(), kGroupThreads>(a, it, in_s, gt);
       if (lane == 0) {
         // fold the group's warps; the last one publishes the item
         atomicMax(&ctl->gmax[g][k], m);
@@ -1423,11 +1425,230 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         __threadfence_block();
         __syncwarp();
       }
-      enc_key_item<TIn>(a, it, in_s, gt, lane, ctl->layer_max, release, released);
+      enc_key_item<TIn, enc_chunk<TIn>(), kGroupThreads>(a, it, in_s, gt, lane, ctl->layer_max, release, released);
     } else {
-      enc_value_item<D, TIn, SYM, SIGN>(a, it, in_s, wig, lane, R, C);
+      enc_value_item<D, TIn, SYM, SIGN, enc_chunk<TIn>(), kWarpsPerGroup>(a, it, in_s, wig, lane, R, C);
     }
     if (!released) release();  // this warp is done with the stage
+  }
+}
+
+// ---------------------------------------------------------------------------
+// encode kernel, co-resident roles (every SM runs values AND keys)
+// ---------------------------------------------------------------------------
+// The role-split enc_kernel pays the SM-time of both roles in sequence: the
+// value role is bound by instruction issue (register reads) and the key role
+// by memory latency, on disjoint SMs. Here every CTA (one per SM) runs both,
+// on different SM sub-partitions so that no SMSP's L0 instruction cache holds
+// both code paths (warp w issues on SMSP w % 4; mixing the two paths on one
+// SMSP thrashed it, 33% no_instructions):
+//   group g = SMSP g: warps {g, g + 4, g + 8} (warp 0 is the TMA producer,
+//   so group 0 is warps 4, 8, 12);
+//   groups 0-2: value items, group 3: absmax + key-encode items.
+// The key group's memory latency hides under the value groups' ALU work.
+// Items: bf16 12288 / f32 6144 elements (24 KB stages, two per group); a
+// value item is two (d=128) passes of the group's three warps.
+constexpr int kCoWPG = 3;
+constexpr int kCoGT = 32 * kCoWPG;
+constexpr int kCoGroups = 4;
+constexpr int kCoThreads = 32 + kCoGroups * kCoGT;  // 416: 13 warps
+constexpr int kCoStage = 24 * 1024;
+constexpr int kCoNSG = 2;
+template <typename TIn>
+constexpr int co_chunk() {
+  return kCoStage / (int)sizeof(TIn);
+}
+inline int co_chunk_for(int elem_bytes) { return kCoStage / elem_bytes; }
+
+template <int D>
+constexpr size_t co_smem_bytes() {
+  return 1024 + (size_t)kCoGroups * kCoNSG * kCoStage + sizeof(Ctl) + (size_t)12 * (D * 8 + D);
+}
+
+template <int D, typename TIn, bool SYM, bool SIGN>
+__global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_constant__ EncArgs a) {
+  constexpr int CH = co_chunk<TIn>();
+  using TL = Tile<D, (int)sizeof(TIn), CH, kCoWPG>;
+  constexpr int NG = kCoGroups, NSG = kCoNSG;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = align1024(smem_raw);
+  Ctl* ctl = reinterpret_cast<Ctl*>(ring + NG * NSG * kCoStage);
+  uint8_t* replay_base = reinterpret_cast<uint8_t*>(ctl + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < NG; ++g)
+      for (int k = 0; k < NSG; ++k) {
+        tma::mbar_init(&ctl->full[g][k], 1);
+        tma::mbar_init(&ctl->empty[g][k], kCoWPG);  // every warp of the group releases
+      }
+    tma::fence_mbar_init();
+  }
+  if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
+  if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
+  if (threadIdx.x < kMaxGroups * kMaxSG) {
+    (&ctl->gmax[0][0])[threadIdx.x] = 0;
+    (&ctl->gcnt[0][0])[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  // role of group g: true = values
+  auto value_group = [&](int g) { return a.co_roles == 1 || (a.co_roles == 0 && g < 3); };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_first = tma::policy_evict_first(), pol_last = tma::policy_evict_last();
+      auto issue = [&](const Item& it, uint8_t* dst, uint64_t* bar) {
+        if (it.kind == kValEnc) {
+          tma::mbar_arrive_expect_tx(bar, (uint32_t)(CH * (int)sizeof(TIn)));
+          const int row0 = it.idx * TL::VR;
+#pragma unroll 1
+          for (int rb = 0; rb < TL::NRB; ++rb)
+#pragma unroll 1
+            for (int cb = 0; cb < TL::NCB; ++cb)
+              tma::tensor2d_g2s(dst + (rb * TL::NCB + cb) * TL::BOX_BYTES, &a.tm_v[it.layer],
+                                cb * (TL::IB / (int)sizeof(TIn)), row0 + rb * TL::BR, bar, pol_first);
+        } else {
+          const long long e0 = (long long)it.idx * CH;
+          const uint32_t bytes = (uint32_t)(min((long long)CH, a.nelem - e0) * (long long)sizeof(TIn));
+          tma::mbar_arrive_expect_tx(bar, bytes);
+          tma::bulk_g2s(dst, static_cast<const TIn*>(a.k_in[it.layer]) + e0, bytes, bar,
+                        it.kind == kAbsmax ? pol_last : pol_first);
+        }
+      };
+      // ---- value cursor: this CTA's static slice of the layer-major V list ----
+      const long long G = gridDim.x;
+      const long long totV = (long long)a.num_layers * a.nV;
+      long long tv = blockIdx.x;
+      auto next_value = [&]() -> Item {
+        if (tv >= totV) return Item{kEnd, 0, 0, 0};
+        const Item it = enc_value_item_at(a, tv);
+        tv += G;
+        return it;
+      };
+      // ---- key cursor: absmax items A and key-encode items E (see enc_kernel);
+      // never blocks (returns kNone), so the value groups keep being fed ----
+      const uint32_t GK = gridDim.x;
+      const uint32_t nA = (uint32_t)a.nA, nE = (uint32_t)a.nE;
+      const uint32_t totA = (uint32_t)a.num_layers * nA, totE = (uint32_t)a.num_layers * nE;
+      uint32_t ta = blockIdx.x, te = blockIdx.x;
+      int ready = -1, polled = -1, pending = -1;
+      uint32_t polled_cnt = 0, pending_max = 0;
+      const bool tensor_keys = nA > 0;
+      auto next_key = [&]() -> Item {
+        for (;;) {
+          if (te >= totE) return Item{kEnd, 0, 0, 0};
+          const int el = (int)(te / nE);
+          if (!tensor_keys || el <= ready) {
+            const Item it{kKeyEnc, el, (int)(te - (uint32_t)el * nE), 0};
+            te += GK;
+            return it;
+          }
+          if (pending == el) {
+            ctl->layer_max[el] = pending_max;
+            __threadfence_block();
+            *reinterpret_cast<volatile uint32_t*>(&ctl->ready[el]) = 1u;
+            ready = el;
+            continue;
+          }
+          if (polled == el && polled_cnt >= nA) {
+            fence_acq_rel_gpu();
+            pending_max = ld_relaxed_u32(a.layer_max + el);  // staged at the next call
+            pending = el;
+          } else {
+            polled = el;
+            polled_cnt = ld_relaxed_u32(a.layer_done + el);  // consumed at the next call
+          }
+          if (ta < totA && (int)(ta / nA) < el + a.key_lag) {
+            const int al = (int)(ta / nA);
+            const Item it{kAbsmax, al, (int)(ta - (uint32_t)al * nA), 0};
+            ta += GK;
+            return it;
+          }
+          return Item{kNone, 0, 0, 0};
+        }
+      };
+      // ---- per-group rings; kNone = nothing for this group right now ----
+      int head[NG];
+      bool ended[NG];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        head[g] = 0;
+        ended[g] = false;
+      }
+      int ends = 0;
+      uint32_t spins = 0;
+      uint64_t t0 = 0;
+      while (ends < NG) {
+        bool any = false;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          if (ended[g]) continue;
+          const int k = head[g] % NSG, use = head[g] / NSG;
+          if (use >= 1 && !tma::mbar_test_wait(&ctl->empty[g][k], (uint32_t)(use - 1) & 1u)) continue;
+          Item it;
+          if (value_group(g)) {
+            it = next_value();
+          } else {
+            it = next_key();
+            if (it.kind == kNone) continue;
+          }
+          ctl->items[g][k] = it;
+          ++head[g];
+          any = true;
+          if (it.kind == kEnd) {
+            tma::mbar_arrive(&ctl->full[g][k]);
+            ended[g] = true;
+            ++ends;
+            continue;
+          }
+          issue(it, ring + (g * NSG + k) * kCoStage, &ctl->full[g][k]);
+        }
+        if (!any) {
+          __nanosleep(32);
+          tma::watchdog(spins, t0);  // traps only after ~10 s without progress
+        } else {
+          spins = 0;
+          t0 = 0;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: group = SMSP ----------------
+  const int g = warp & 3;
+  const int wig = (warp - 1) >> 2;  // 0..2 (warp 4 -> 0 for group 0)
+  const int gt = wig * 32 + lane;
+  double* R = reinterpret_cast<double*>(replay_base) + (warp - 1) * D;
+  uint8_t* C = replay_base + 12 * D * 8 + (warp - 1) * D;
+  for (int n = 0;; ++n) {
+    const int k = n % NSG;
+    tma::mbar_wait(&ctl->full[g][k], (uint32_t)(n / NSG) & 1u);
+    const Item it = ctl->items[g][k];
+    if (it.kind == kEnd) break;
+    const uint32_t in_s = tma::smem_u32(ring + (g * NSG + k) * kCoStage);
+    bool released = false;
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&ctl->empty[g][k]);
+    };
+    if (it.kind == kAbsmax) {
+      const uint32_t m = enc_absmax_item<TIn, CH, kCoGT>(a, it, in_s, gt);
+      if (lane == 0) {
+        atomicMax(&ctl->gmax[g][k], m);
+        __threadfence_block();
+        if (atomicAdd(&ctl->gcnt[g][k], 1u) == kCoWPG - 1) {
+          const uint32_t gm = atomicExch(&ctl->gmax[g][k], 0u);
+          ctl->gcnt[g][k] = 0;
+          if (gm) atomicMax(a.layer_max + it.layer, gm);
+          red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
+        }
+      }
+    } else if (it.kind == kKeyEnc) {
+      enc_key_item<TIn, CH, kCoGT>(a, it, in_s, gt, lane, ctl->layer_max, release, released);
+    } else {
+      enc_value_item<D, TIn, SYM, SIGN, CH, kCoWPG>(a, it, in_s, wig, lane, R, C);
+    }
+    if (!released) release();
   }
 }
 
@@ -1583,7 +1804,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec, int chunk) {
   auto fn = encode_fn();
   if (!fn) return false;
-  const int RB = D * eb, IB = RB < 128 ? RB : 128, VR = chunk / D, BR = VR < 256 ? VR : 256;
+  const int RB = D * eb, IB = RB < 128 ? RB : 128, VR = chunk / D, BR = VR / ((VR + 255) / 256);  // == Tile::BR
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)nvec};
   cuuint64_t strides[1] = {(cuuint64_t)RB};
   cuuint32_t box[2] = {(cuuint32_t)(IB / eb), (cuuint32_t)BR};
@@ -1631,6 +1852,26 @@ int enc_launch(const EncArgs& a, int d, bool sym, bool sign, cudaStream_t st) {
     case 32: return enc_launch_d<32, TIn>(a, sym, sign, st);
     case 64: return enc_launch_d<64, TIn>(a, sym, sign, st);
     case 128: return enc_launch_d<128, TIn>(a, sym, sign, st);
+    default: return PKV_ERR_UNSUPPORTED_HEAD_DIM;
+  }
+}
+
+template <int D, typename TIn>
+int co_launch_d(const EncArgs& a, bool sym, bool sign, cudaStream_t st) {
+  const size_t smem = co_smem_bytes<D>();
+  if (sym) {
+    return sign ? coop_launch(enc_co_kernel<D, TIn, true, true>, &a, smem, kCoThreads, st)
+                : coop_launch(enc_co_kernel<D, TIn, true, false>, &a, smem, kCoThreads, st);
+  }
+  return sign ? coop_launch(enc_co_kernel<D, TIn, false, true>, &a, smem, kCoThreads, st)
+              : coop_launch(enc_co_kernel<D, TIn, false, false>, &a, smem, kCoThreads, st);
+}
+
+template <typename TIn>
+int co_launch(const EncArgs& a, int d, bool sym, bool sign, cudaStream_t st) {
+  switch (d) {
+    case 64: return co_launch_d<64, TIn>(a, sym, sign, st);
+    case 128: return co_launch_d<128, TIn>(a, sym, sign, st);
     default: return PKV_ERR_UNSUPPORTED_HEAD_DIM;
   }
 }
@@ -1692,7 +1933,12 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
   std::memcpy(a->sign_bits, r.sign_bits, sizeof(a->sign_bits));
   a->status = r.status;
   a->replay_count = r.replay_count;
-  const int kEncChunk = enc_chunk_for(eb);
+  // role-split kernel by default; PKV_ENC_ROLES=co selects the co-resident
+  // one (head_dim 64 / 128), measured slower: C3 f32 507 vs 320 us, bf16 399
+  // vs 253 us -- one 3-warp key group per SM keeps too few key bytes in
+  // flight (48 KB) and the 3-warp value groups lose ~4%
+  const bool co = tuning().enc_co && (!do_v || r.head_dim == 64 || r.head_dim == 128);
+  const int kEncChunk = co ? co_chunk_for(eb) : enc_chunk_for(eb);
   const long long kch = (nelem + kEncChunk - 1) / kEncChunk;
   const long long vr = kEncChunk / std::max(r.head_dim, 1);
   a->nE = do_k ? (int)kch : 0;
@@ -1789,8 +2035,16 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       key_ctas = grid;
     }
     a->value_ctas = grid - key_ctas;
-    rc = eb == 4 ? enc_launch<float>(*a, dk, r.cb.symmetric != 0, r.sign, st)
-                 : enc_launch<__nv_bfloat16>(*a, dk, r.cb.symmetric != 0, r.sign, st);
+    if (co) {
+      a->co_roles = (do_k && do_v) ? 0 : (do_v ? 1 : 2);
+      a->value_ctas = grid;
+      a->abs_lead = 0;
+      rc = eb == 4 ? co_launch<float>(*a, dk, r.cb.symmetric != 0, r.sign, st)
+                   : co_launch<__nv_bfloat16>(*a, dk, r.cb.symmetric != 0, r.sign, st);
+    } else {
+      rc = eb == 4 ? enc_launch<float>(*a, dk, r.cb.symmetric != 0, r.sign, st)
+                   : enc_launch<__nv_bfloat16>(*a, dk, r.cb.symmetric != 0, r.sign, st);
+    }
   }
   delete a;
   return rc;

@@ -13,6 +13,7 @@ struct Tuning {
   bool codec_warp = false;         // PKV_CODEC_PATH=warp: warp-granular codec (codec.cu) only
   int dbg_enc = 0;                 // PKV_DBG_ENC: encode timing experiments (skip math)
   int key_lag = 0;                 // PKV_KEY_LAG (0 = default): absmax layers ahead of the key encode
+  bool enc_co = false;             // PKV_ENC_ROLES=co: co-resident encode roles (enc_co_kernel) instead of SM role split
   bool abs_on_values = false;      // PKV_ABSMAX_ROLE=values: per-tensor key absmax items run on the value CTAs
   double key_sm_fraction = -1.0;   // PKV_KEY_SM_FRACTION (<0 = default): encode SMs for the key role
   double dec_key_fraction = -1.0;  // PKV_DEC_KEY_FRACTION (<0 = default): decode SMs for key items

@@ -379,10 +379,15 @@ def test_role_splits_and_schedules_do_not_change_results(monkeypatch, mode):
     dump = pk.synth_gaussian_dump(g, seed=11, device="cuda", dtype=torch.bfloat16, generator="torch")
     ref = pk.build_pool(dump, k_scale_mode=mode)
     ref_out = ref.attach(16).materialize_all()
-    for enc_frac, dec_frac, lag in [("0.1", "0.1", "1"), ("0.6", "0", "2"), ("0.9", "0.9", "8")]:
+    # (also the co-resident encode kernel, PKV_ENC_ROLES=co, against the
+    # default role-split one; SM shares only matter to the split kernel)
+    for enc_frac, dec_frac, lag, roles in [("0.1", "0.1", "1", "split"), ("0.6", "0", "2", "split"),
+                                           ("0.9", "0.9", "8", "split"), ("0.3", "0.3", "1", "co"),
+                                           ("0.3", "0.3", "7", "co")]:
         monkeypatch.setenv("PKV_KEY_SM_FRACTION", enc_frac)
         monkeypatch.setenv("PKV_DEC_KEY_FRACTION", dec_frac)
         monkeypatch.setenv("PKV_KEY_LAG", lag)
+        monkeypatch.setenv("PKV_ENC_ROLES", roles)
         _lib.reload_tuning()  # knobs are read once per process otherwise
         p = pk.build_pool(dump, k_scale_mode=mode)
         for i in range(g.num_layers):
