@@ -294,14 +294,20 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
-    if torch.cuda.device_count() <= local:
+    plumbing = args.dist_backend == "gloo"  # N>1 code path on fewer GPUs: exercises, does not measure
+    if torch.cuda.device_count() <= local and not plumbing:
         raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible")
+    if plumbing:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log (nRanks)
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if plumbing:
+            dist.init_process_group("gloo")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log (nRanks)
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
     g = pk.ModelGeometry(num_layers=L, kv_heads=H, head_dim=D, seq_len=T)
     mine = list(parallel.layer_shard(L, world, rank))
     my_agents = parallel.partition_agents(agents, world, rank)
@@ -373,8 +379,10 @@ def run_ours(args, cfg):
         def gather():
             if world > 1:
                 arena.status_row.copy_(arena.status)
-                if even:
+                if even and not plumbing:
                     dist.all_gather_into_tensor(full_flat, arena.flat)
+                elif even:
+                    full_flat.copy_(parallel.gather_arena(arena, L).flat)
                 else:
                     parallel.gather_arena(arena, L)
 
@@ -393,8 +401,10 @@ def run_ours(args, cfg):
             decode()
         raise_for_status(arena.status)
         torch.cuda.synchronize(dev)
-        run_enc, run_gat, run_dec = capture(encode) or encode, (capture(gather) if even else None) or gather, \
-            capture(decode) or decode
+        # (the all-gather runs eager: one NCCL call per step; capturing a
+        # collective is not needed to time it and a failed capture must not
+        # disturb the encode / decode graphs)
+        run_enc, run_gat, run_dec = capture(encode) or encode, gather, capture(decode) or decode
         graphed = not args.no_graph and run_enc is not encode
         for _ in range(args.warmup):
             run_enc()
@@ -621,6 +631,8 @@ def run_ours(args, cfg):
                f"(replicated on every GPU) + materialise of each GPU's layers; decode agents partitioned "
                f"{[len(parallel.partition_agents(agents, world, x)) for x in range(world)]}")
         line = {
+            **({"plumbing_test": "gloo backend, ranks share GPUs: a code-path check, not a measurement"}
+               if plumbing else {}),
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": f"{dtn} in / u8+int8 pool / bf16 out",
@@ -707,6 +719,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graphs")
     ap.add_argument("--skip-decode-e2e", action="store_true", help="skip the model-level decode measurement")
     ap.add_argument("--skip-variant", action="store_true", help="skip the other input dtype's measurement")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N>1 path with ranks sharing the visible GPUs (plumbing check only)")
     ap.add_argument("--plan-only", action="store_true",
                     help="print each rank's layer / agent shard (gloo; no GPU work) and exit")
     args = ap.parse_args()

@@ -434,6 +434,23 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     const __half lc = __float2half_rn(a.cent32[k] - __half2float(hc));
     ctab[k * 128 + tid] = (uint32_t)__half_as_ushort(hc) | ((uint32_t)__half_as_ushort(lc) << 16);
   }
+  const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 1.f;
+  // raw tile layout: int8 codes [TT][D] | packed values [TT][3D/8] | f32 scales [TT]
+  auto stage = [&](long long t0, int nt, uint8_t* buf) {
+    const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
+    for (int i = tid; i < nt * D / 16; i += 128) cp_async16(buf + i * 16, gk + i * 16);
+    const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
+    uint8_t* bv = buf + TT * D;
+    for (int i = tid; i < nt * (3 * D / 8) / 4; i += 128) cp_async4(bv + i * 4, gv + i * 4);
+    const float* gs = a.v_scales + (long long)h * a.T + t0;
+    float* bs = reinterpret_cast<float*>(buf + TT * D + TT * 3 * D / 8);
+    for (int i = tid; i < nt; i += 128) cp_async4(bs + i, gs + i);
+    cp_async_commit();
+  };
+  // two tiles in flight: tile i + 1 loads while tile i converts and computes
+  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT, t_end - t_begin), raw0);
+  if (t_begin + TT < t_end) stage(t_begin + TT, (int)min((long long)TT, t_end - t_begin - TT), raw0 + MT::RAW);
+  // (Q is loaded while the first two tiles are in flight)
   // ---- Q tile (x qscale), split hi / lo, f16 swizzled [RT][D] ----
   for (int i = tid; i < RT * D / 8; i += 128) {
     const int r = i / (D / 8), c = i % (D / 8);
@@ -463,23 +480,6 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     *reinterpret_cast<uint4*>(qhi + sw<D>(r, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     *reinterpret_cast<uint4*>(qlo + sw<D>(r, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
-  const float ts = a.k_mode == PKV_K_TENSOR ? __ldg(a.k_scale) : 1.f;
-
-  // raw tile layout: int8 codes [TT][D] | packed values [TT][3D/8] | f32 scales [TT]
-  auto stage = [&](long long t0, int nt, uint8_t* buf) {
-    const int8_t* gk = a.k_codes + ((long long)h * a.T + t0) * D;
-    for (int i = tid; i < nt * D / 16; i += 128) cp_async16(buf + i * 16, gk + i * 16);
-    const uint8_t* gv = a.v_packed + ((long long)h * a.T + t0) * (3 * D / 8);
-    uint8_t* bv = buf + TT * D;
-    for (int i = tid; i < nt * (3 * D / 8) / 4; i += 128) cp_async4(bv + i * 4, gv + i * 4);
-    const float* gs = a.v_scales + (long long)h * a.T + t0;
-    float* bs = reinterpret_cast<float*>(buf + TT * D + TT * 3 * D / 8);
-    for (int i = tid; i < nt; i += 128) cp_async4(bs + i, gs + i);
-    cp_async_commit();
-  };
-  // two tiles in flight: tile i + 1 loads while tile i converts and computes
-  if (t_begin < t_end) stage(t_begin, (int)min((long long)TT, t_end - t_begin), raw0);
-  if (t_begin + TT < t_end) stage(t_begin + TT, (int)min((long long)TT, t_end - t_begin - TT), raw0 + MT::RAW);
 
   float o[ND][4];
 #pragma unroll
@@ -625,8 +625,9 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     }
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
-      o[j][0] *= corr[0]; o[j][1] *= corr[0];
-      o[j][2] *= corr[1]; o[j][3] *= corr[1];
+      float2 lo = __fmul2_rn(make_float2(o[j][0], o[j][1]), make_float2(corr[0], corr[0]));
+      float2 hi = __fmul2_rn(make_float2(o[j][2], o[j][3]), make_float2(corr[1], corr[1]));
+      o[j][0] = lo.x; o[j][1] = lo.y; o[j][2] = hi.x; o[j][3] = hi.y;
     }
     // ---- O += P' (Y_hi + Y_lo) over the warp's tokens, 16 tokens per k-step ----
 #pragma unroll
