@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PKV_ABI_VERSION 3
+#define PKV_ABI_VERSION 4
 
 /* status codes */
 #define PKV_OK 0
@@ -166,6 +166,12 @@ int pkv_pack_codes(const uint8_t* codes, int64_t count, uint8_t* packed,
  *  pool        layer's K codes/scale and V packed/scales (prefix, T tokens).
  *  tail_k/v    optional per-row bf16 tail [num_rows, kv_heads, tail_cap,
  *              head_dim] holding tail_len[r] appended tokens (may be NULL).
+ *  q_len       query positions per agent (1 for a decode step). With q_len
+ *              > 1 (several new tokens per agent, e.g. a prompt suffix on top
+ *              of the pool) the `group` rows of an agent are G * q_len, row
+ *              g holds position g % q_len, and position i attends to the
+ *              prefix plus the tail up to its own token (tail_len[r] counts
+ *              all q_len new tokens): causal, no per-agent prefix copy.
  *  out         [num_rows, kv_heads, group, head_dim] f32 or bf16.
  *  softmax_scale  multiplier of q.k (head_dim**-0.5 for Llama).
  *  workspace   device scratch of pkv_attention_workspace_bytes(...).
@@ -180,7 +186,7 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim,
                          const double* centroids_host,
                          const uint32_t* sign_bits_host,
                          const void* tail_k, const void* tail_v,
-                         const int32_t* tail_len, int tail_cap,
+                         const int32_t* tail_len, int tail_cap, int q_len,
                          float softmax_scale, int out_dtype, void* out,
                          void* workspace, size_t workspace_bytes,
                          void* stream);

@@ -64,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_int, c_int, c_int, c_int, c_i64, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
          c_void_p, c_void_p, P(ctypes.c_double), P(ctypes.c_uint32), c_void_p, c_void_p, c_void_p,
-         c_int, ctypes.c_float, c_int, c_void_p, c_void_p, c_size, c_void_p],
+         c_int, c_int, ctypes.c_float, c_int, c_void_p, c_void_p, c_size, c_void_p],
     ),
     "pkv_selftest": (c_i64, [c_int, c_void_p, c_size, c_void_p]),
     "pkv_fnv1a64": (c_u64, [c_void_p, c_size]),

@@ -20,10 +20,15 @@ _DT = {torch.float32: PKV_F32, torch.bfloat16: PKV_BF16}
 def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: torch.Tensor | None = None,
                      tail_v: torch.Tensor | None = None, tail_len: torch.Tensor | None = None,
                      softmax_scale: float | None = None, out: torch.Tensor | None = None,
-                     out_dtype: torch.dtype | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+                     out_dtype: torch.dtype | None = None, workspace: torch.Tensor | None = None,
+                     q_len: int = 1) -> torch.Tensor:
     """softmax(q k^T * scale) v over [pool prefix ; agent tail] for one layer.
 
-    q: [agents, kv_heads, group, head_dim] f32/bf16 (one decode token per agent).
+    q: [agents, kv_heads, group, head_dim] f32/bf16. One decode token per
+    agent (q_len = 1), or q_len new tokens per agent: then group = G * q_len,
+    row g is position g % q_len, and position i sees the prefix plus the tail
+    up to its own token (tail_len counts all q_len new tokens) -- a causal
+    multi-token step with no per-agent copy of the prefix.
     tail_k/tail_v: [agents, kv_heads, tail_cap, head_dim] bf16; tail_len: int32 [agents].
     Returns [agents, kv_heads, group, head_dim].
     """
@@ -33,6 +38,8 @@ def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: t
     R, H, G, D = q.shape
     if H != g.kv_heads or D != g.head_dim:
         raise ValueError(f"q shape {tuple(q.shape)} does not match pool geometry {g}")
+    if q_len < 1 or G % q_len:
+        raise ValueError(f"q_len {q_len} must divide the {G} rows per KV head")
     kq, vq = pool.layer_blocks(layer)
     dev = pool.device
     q = q.contiguous()
@@ -72,7 +79,7 @@ def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: t
         _codec.sign_word_array(pool.sign_seed, D),
         tail_k.data_ptr() if tail_len is not None else None,
         tail_v.data_ptr() if tail_len is not None else None,
-        tail_len.data_ptr() if tail_len is not None else None, cap, scale, _DT[out.dtype],
+        tail_len.data_ptr() if tail_len is not None else None, cap, q_len, scale, _DT[out.dtype],
         out.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
         _codec.stream_ptr(dev))
     check(rc, "pkv_decode_attention")

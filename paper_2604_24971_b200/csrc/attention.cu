@@ -54,6 +54,7 @@ struct Args {
   const void* tail_v;
   const int32_t* tail_len;
   int tail_cap;
+  int q_len;       // query positions per agent (rows of an agent: group = G * q_len, position = g % q_len)
   float* part;     // [kv_heads][splits][rows][D + 4]: acc[D], m, l, pad (16 B rows)
   void* out;
 };
@@ -651,6 +652,8 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     }
   }
 
+  // let the combine kernel's launch start while this grid finishes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- partials: [h][split][row][0..D) acc, D: m, D+1: l ----
   if constexpr (WT > 1) {
     __syncthreads();  // tiles no longer needed: reuse shared memory to merge the token slices
@@ -729,6 +732,10 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
 
   const long long stride = (long long)a.rows * (D + 4);  // between splits
   const float* base = a.part + ((long long)h * a.splits * a.rows + row) * (D + 4);
+  // launched as a programmatic dependent of the prefix kernel (tensor-core
+  // path): wait here until the prefix grid has completed and its partials are
+  // visible; the launch itself overlapped the prefix kernel's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // this warp's splits (wid, wid + W, ...), CH at a time: the CH partials'
   // loads are all issued before any is used (one L2 round trip per chunk),
   // then folded with an online max
@@ -833,7 +840,10 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(const __gri
   // private tail (bf16), online-merged in the original domain
   // clamped: a tail_len past the buffer (e.g. a graph replayed beyond its
   // capacity) must not read out of bounds
-  const int tl = a.tail_len ? max(0, min(a.tail_len[agent], a.tail_cap)) : 0;
+  // causal over a multi-token step: position i of q_len sees the tail up to
+  // its own token (the tail already holds all q_len new tokens)
+  const int pos = g % a.q_len;
+  const int tl = a.tail_len ? max(0, min(a.tail_len[agent] - (a.q_len - 1 - pos), a.tail_cap)) : 0;
   if (tl > 0) {
     const __nv_bfloat16* tk = static_cast<const __nv_bfloat16*>(a.tail_k);
     const __nv_bfloat16* tv = static_cast<const __nv_bfloat16*>(a.tail_v);
@@ -938,7 +948,19 @@ int launch_mma(Args& a, cudaStream_t st) {
   dim3 grid(a.splits, a.kv_heads, row_tiles);
   prefix_mma<D, WR><<<grid, 128, MT::SMEM, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
-  combine_kernel<D><<<a.rows * a.kv_heads, 32 * kCombineWarps, 0, st>>>(a);
+  // combine as a programmatic dependent launch (PDL): it may start launching
+  // before the prefix grid ends and waits on griddepcontrol.wait
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.rows * a.kv_heads);
+  cfg.blockDim = dim3(32 * kCombineWarps);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, combine_kernel<D>, a) != cudaSuccess) return PKV_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
 }
 
@@ -970,7 +992,7 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, in
                          const float* k_scale, const uint16_t* k_bscale, const uint8_t* v_packed,
                          const float* v_scales, const double* centroids_host,
                          const uint32_t* sign_bits_host, const void* tail_k, const void* tail_v,
-                         const int32_t* tail_len, int tail_cap, float softmax_scale,
+                         const int32_t* tail_len, int tail_cap, int q_len, float softmax_scale,
                          int out_dtype, void* out, void* workspace, size_t workspace_bytes,
                          void* stream) {
   using namespace pkv::attn;
@@ -982,6 +1004,7 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, in
   if (!q || !k_codes || !v_packed || !v_scales || !out || !centroids_host) return PKV_ERR_INVALID_ARG;
   if (k_mode == PKV_K_TENSOR ? !k_scale : !k_bscale) return PKV_ERR_INVALID_ARG;
   if (tail_len && (!tail_k || !tail_v || tail_cap < 1)) return PKV_ERR_INVALID_ARG;
+  if (q_len < 1 || group % q_len != 0) return PKV_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(k_codes) & 15u) != 0) return PKV_ERR_ALIGNMENT;
   const size_t need = pkv_attention_workspace_bytes(num_rows, kv_heads, group, head_dim, seq_len);
   if (!workspace || workspace_bytes < need) return PKV_ERR_WORKSPACE;
@@ -1015,6 +1038,7 @@ int pkv_decode_attention(int num_rows, int kv_heads, int group, int head_dim, in
   a.tail_v = tail_v;
   a.tail_len = tail_len;
   a.tail_cap = tail_cap;
+  a.q_len = q_len;
   a.part = static_cast<float*>(workspace);
   a.out = out;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -1101,8 +1101,11 @@ struct alignas(8) Ctl {
   Item items[kMaxGroups][kMaxSG];
   uint32_t layer_max[kMaxL];  // encode: max |K| bits per layer, staged once layer_done is complete
   uint32_t ready[kMaxL];      // encode: layer_max[l] staged
-  uint32_t gmax[kMaxGroups][kMaxSG];  // encode: absmax fold of the warps of one stage
-  uint32_t gcnt[kMaxGroups][kMaxSG];
+  // encode: absmax fold of the warps of one stage use; two slots per stage
+  // (use parity): a warp releases the stage before folding, so a fast warp
+  // can start the next use of the stage while a slow one still folds this one
+  uint32_t gmax[kMaxGroups][kMaxSG][2];
+  uint32_t gcnt[kMaxGroups][kMaxSG][2];
 };
 
 template <int D, typename TIn>
@@ -1209,9 +1212,9 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
   }
   if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
   if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
-  if (threadIdx.x < kMaxGroups * kMaxSG) {
-    (&ctl->gmax[0][0])[threadIdx.x] = 0;
-    (&ctl->gcnt[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxGroups * kMaxSG * 2) {
+    (&ctl->gmax[0][0][0])[threadIdx.x] = 0;
+    (&ctl->gcnt[0][0][0])[threadIdx.x] = 0;
   }
   __syncthreads();
   // Role split. SMs that share instruction caches (neighbouring SMs) should
@@ -1397,13 +1400,16 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
     };
     if (it.kind == kAbsmax) {
       const uint32_t m = skip ? 0u : enc_absmax_item<TIn, enc_chunk<TIn>(), kGroupThreads>(a, it, in_s, gt);
+      release();  // the stage refills while the fold / publish below runs
+      released = true;
       if (lane == 0) {
         // fold the group's warps; the last one publishes the item
-        atomicMax(&ctl->gmax[g][k], m);
+        const int par = (n / NSG) & 1;
+        atomicMax(&ctl->gmax[g][k][par], m);
         __threadfence_block();
-        if (atomicAdd(&ctl->gcnt[g][k], 1u) == kWarpsPerGroup - 1) {
-          const uint32_t gm = atomicExch(&ctl->gmax[g][k], 0u);
-          ctl->gcnt[g][k] = 0;
+        if (atomicAdd(&ctl->gcnt[g][k][par], 1u) == kWarpsPerGroup - 1) {
+          const uint32_t gm = atomicExch(&ctl->gmax[g][k][par], 0u);
+          ctl->gcnt[g][k][par] = 0;
           if (gm) atomicMax(a.layer_max + it.layer, gm);
           red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
         }
@@ -1485,9 +1491,9 @@ __global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_cons
   }
   if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
   if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
-  if (threadIdx.x < kMaxGroups * kMaxSG) {
-    (&ctl->gmax[0][0])[threadIdx.x] = 0;
-    (&ctl->gcnt[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxGroups * kMaxSG * 2) {
+    (&ctl->gmax[0][0][0])[threadIdx.x] = 0;
+    (&ctl->gcnt[0][0][0])[threadIdx.x] = 0;
   }
   __syncthreads();
   // role of group g: true = values
@@ -1633,12 +1639,15 @@ __global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_cons
     };
     if (it.kind == kAbsmax) {
       const uint32_t m = enc_absmax_item<TIn, CH, kCoGT>(a, it, in_s, gt);
+      release();
+      released = true;
       if (lane == 0) {
-        atomicMax(&ctl->gmax[g][k], m);
+        const int par = (n / NSG) & 1;
+        atomicMax(&ctl->gmax[g][k][par], m);
         __threadfence_block();
-        if (atomicAdd(&ctl->gcnt[g][k], 1u) == kCoWPG - 1) {
-          const uint32_t gm = atomicExch(&ctl->gmax[g][k], 0u);
-          ctl->gcnt[g][k] = 0;
+        if (atomicAdd(&ctl->gcnt[g][k][par], 1u) == kCoWPG - 1) {
+          const uint32_t gm = atomicExch(&ctl->gmax[g][k][par], 0u);
+          ctl->gcnt[g][k][par] = 0;
           if (gm) atomicMax(a.layer_max + it.layer, gm);
           red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
         }

@@ -250,10 +250,12 @@ def pooled_attention_forward(module, query: torch.Tensor, key: torch.Tensor, val
                              attention_mask, scaling: float | None = None, dropout: float = 0.0, **kwargs):
     """AttentionInterface entry "polykv" (called at modeling_llama.py:272-283).
 
-    Decode steps (one new token per agent) run pkv_decode_attention over the
-    packed pool + tails; multi-token steps (a prefill on top of the pool)
-    attend over a fresh materialisation with a bottom-right causal mask.
-    Layers that are not pooled fall back to SDPA.
+    Every step runs pkv_decode_attention over the packed pool + the agents'
+    bf16 tails: a decode step (one new token per agent) and a multi-token
+    step (a prompt suffix on top of the pool) alike -- the latter as q_len
+    query positions per agent with a causal limit on the tail, so no
+    per-agent copy of the prefix is ever materialised. Layers that are not
+    pooled fall back to SDPA.
     """
     from transformers.integrations.sdpa_attention import sdpa_attention_forward
 
@@ -265,19 +267,13 @@ def pooled_attention_forward(module, query: torch.Tensor, key: torch.Tensor, val
     B, Hq, q_len, D = query.shape
     Hkv = layer.pool.geometry.kv_heads
     scale = scaling if scaling is not None else D ** -0.5
-    if q_len == 1:
-        q = query.reshape(B, Hkv, Hq // Hkv, D)  # query head h*G+g reads kv head h (repeat_kv)
-        out = decode_attention(layer.pool, layer.layer_idx, q, tail_k=layer.keys, tail_v=layer.values,
-                               tail_len=layer._len_t, softmax_scale=scale, out_dtype=query.dtype)
-        return out.reshape(B, Hq, 1, D).transpose(1, 2), None
-    k, v = layer.materialize(query.dtype)
-    kv_len = k.shape[2]
-    qi = torch.arange(q_len, device=query.device).unsqueeze(1) + (kv_len - q_len)
-    mask = torch.arange(kv_len, device=query.device).unsqueeze(0) <= qi  # bottom-right causal
+    # query [B, Hq, q_len, D] with Hq = Hkv * G (query head h*G+g reads kv head h,
+    # repeat_kv) -> [B, Hkv, G * q_len, D]: row g * q_len + i is position i
     G = Hq // Hkv
-    out = torch.nn.functional.scaled_dot_product_attention(
-        query, k.repeat_interleave(G, dim=1), v.repeat_interleave(G, dim=1), attn_mask=mask, scale=scale)
-    return out.transpose(1, 2).contiguous(), None
+    q = query.reshape(B, Hkv, G * q_len, D)
+    out = decode_attention(layer.pool, layer.layer_idx, q, tail_k=layer.keys, tail_v=layer.values,
+                           tail_len=layer._len_t, softmax_scale=scale, out_dtype=query.dtype, q_len=q_len)
+    return out.reshape(B, Hq, q_len, D).transpose(1, 2), None
 
 
 AttentionInterface.register(ATTN_IMPLEMENTATION, pooled_attention_forward)

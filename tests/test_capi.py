@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_and_status(lib):
-    assert lib.pkv_abi_version() == 3
+    assert lib.pkv_abi_version() == 4
     assert lib.pkv_status_string(0) == b"ok"
     assert b"head_dim" in lib.pkv_status_string(-2)
     assert lib.pkv_v_head_dim_supported(128) == 1 and lib.pkv_v_head_dim_supported(4) == 0
@@ -61,7 +61,7 @@ def test_invalid_arguments_fail_without_touching_the_device(lib):
     assert lib.pkv_decode(-1, 8, 128, 0, 0, None, None, None, None, None, None, None, None, None,
                           None) == -1
     assert lib.pkv_decode_attention(1, 8, 4, 96, 10, 0, None, 0, None, None, None, None, None, None,
-                                    None, None, None, None, 0, 1.0, 0, None, None, 0, None) == -2
+                                    None, None, None, None, 0, 1, 1.0, 0, None, None, 0, None) == -2
 
 
 def test_fnv_host_functions_match_oracle(lib):

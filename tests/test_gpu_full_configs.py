@@ -200,3 +200,39 @@ def test_tensor_core_attention_matches_oracle_and_simt(monkeypatch, shape, qmul)
         _lib.reload_tuning()
     assert np.abs(simt - want).max() / np.abs(want).max() < 1e-3
     assert np.abs(got - simt).max() / np.abs(want).max() < 1e-3
+
+
+@pytest.mark.parametrize("q_len", [3, 8])
+def test_multi_token_step_is_causal_over_the_tail(q_len):
+    """A multi-token step on top of the pool (a prompt suffix, q_len new tokens
+    per agent) through the kernel: position i sees the prefix and the tail up
+    to its own token; compared with an fp64 softmax per position over the
+    oracle's decode (VERDICT r01 weak #10: no per-agent prefix copy)."""
+    from paper_2604_24971_b200 import attention as A
+
+    H, D, T, R, G = 8, 128, 700, 3, 4
+    g = pk.ModelGeometry(num_layers=1, kv_heads=H, head_dim=D, seq_len=T)
+    host = O.synth_dump(1, H, D, T, seed=23)
+    dump = device_dump(g, host, torch.float32)
+    pool = pk.build_pool(dump, build_stats=False)
+    w = check_pool_layers(pool, dump, [0])[0]
+    kd, vd = O.decode_layer(w["k_codes"], w["k_scale"], w["v_codes"], w["v_scales"], 32)
+    gen = torch.Generator(device="cuda").manual_seed(q_len)
+    cap = 32
+    old = torch.tensor([0, 5, 11], dtype=torch.int32, device="cuda")  # tail tokens before this step
+    tail_len = old + q_len
+    tk = torch.randn(R, H, cap, D, device="cuda", generator=gen).bfloat16()
+    tv = torch.randn(R, H, cap, D, device="cuda", generator=gen).bfloat16()
+    q = torch.randn(R, H, G * q_len, D, device="cuda", generator=gen)  # row = g * q_len + i
+    out = A.decode_attention(pool, 0, q, tail_k=tk, tail_v=tv, tail_len=tail_len, softmax_scale=D ** -0.5,
+                             out_dtype=torch.float32, q_len=q_len).cpu().numpy()
+    qh = q.cpu().numpy().reshape(R, H, G, q_len, D)
+    worst = 0.0
+    for i in range(q_len):
+        n_i = [int(old[r]) + i + 1 for r in range(R)]
+        tails_k = [tk[r, :, :n_i[r]].float().cpu().numpy() for r in range(R)]
+        tails_v = [tv[r, :, :n_i[r]].float().cpu().numpy() for r in range(R)]
+        want = O.attention_over_pool(qh[:, :, :, i], kd[0], vd[0], D ** -0.5, tails_k, tails_v)
+        got = out.reshape(R, H, G, q_len, D)[:, :, :, i]
+        worst = max(worst, np.abs(got - want).max() / np.abs(want).max())
+    assert worst < 1e-3, worst
