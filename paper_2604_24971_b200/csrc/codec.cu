@@ -753,6 +753,117 @@ __global__ void __launch_bounds__(kThreads, 2) decode_kernel(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
+// values at head_dim 1, 2, 4 (legal in the reference: model.py:47-76 only asks
+// for a power of two). One thread per packed 24-bit word, i.e. 8 / d whole
+// vectors; the encode is the exact fp64 computation in numpy's operation
+// order (the same arithmetic as v_replay), the decode the f32 sequence of
+// dequantize_v. A tiny-vector path: these shapes carry no bandwidth.
+// ---------------------------------------------------------------------------
+constexpr int kSmallThreads = 256;
+
+template <typename TIn>
+__global__ void __launch_bounds__(kSmallThreads) v_encode_small_kernel(const __grid_constant__ EncodeArgs a) {
+  const int D = a.head_dim;
+  const long long groups = (a.nelem + 7) / 8;
+  const long long total = groups * a.num_layers;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int layer = (int)(t / groups);
+    const long long g = t - (long long)layer * groups;
+    const TIn* src = static_cast<const TIn*>(a.v_in[layer]);
+    uint32_t word = 0;
+    bool nonfinite = false;
+    for (int e0 = 0; e0 < 8; e0 += D) {
+      const long long v = (g * 8 + e0) / D;
+      if (v >= a.nvec) break;
+      double r[4];
+      for (int i = 0; i < D; ++i) {
+        const double x = (double)load1(src + v * D + i);
+        r[i] = sign_bit(a.sign_bits, i) ? -x : x;  // vals * sign_diagonal
+      }
+      for (int h = 1; h < D; h <<= 1)  // fwht.py:31-39 in f64
+        for (int q = 0; q < D / 2; ++q) {
+          const int i = (q / h) * 2 * h + (q % h);
+          const double lo = r[i], hi = r[i + h];
+          r[i] = __dadd_rn(lo, hi);
+          r[i + h] = __dsub_rn(lo, hi);
+        }
+      const double sq = sqrt((double)D);
+      for (int i = 0; i < D; ++i) r[i] = __ddiv_rn(r[i], sq);  // fwht.py:50
+      const double S = pairwise_sumsq(r, D);  // np.square then the pairwise mean
+      float scale = 0.f;
+      if (!(S <= 1.79e308)) {
+        nonfinite = true;
+      } else {
+        const double rms = sqrt(__ddiv_rn(S, (double)D));
+        scale = (float)rms;
+        const double den = rms > 0.0 ? rms : 1.0;
+        for (int i = 0; i < D; ++i) {
+          const double z = __ddiv_rn(r[i], den);
+          uint32_t c = 0;
+#pragma unroll
+          for (int k = 0; k < 7; ++k) c += (a.cb.mid64[k] < z) ? 1u : 0u;  // searchsorted 'left'
+          if (scale != 0.f) word |= c << (3 * (e0 + i));
+        }
+      }
+      a.v_scales[layer][v] = scale;
+    }
+    if (nonfinite) {
+      word = 0;
+      atomicOr(&a.status[layer], PKV_FLAG_V_NONFINITE);
+    }
+    uint8_t* p = a.v_packed[layer] + 3 * g;
+    p[0] = (uint8_t)(word & 0xff);
+    p[1] = (uint8_t)((word >> 8) & 0xff);
+    p[2] = (uint8_t)((word >> 16) & 0xff);
+  }
+}
+
+template <typename TOut>
+__global__ void __launch_bounds__(kSmallThreads) v_decode_small_kernel(const __grid_constant__ DecodeArgs a) {
+  const int D = a.head_dim;
+  const long long groups = (a.nelem + 7) / 8;
+  const long long total = groups * a.num_layers;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int layer = (int)(t / groups);
+    const long long g = t - (long long)layer * groups;
+    const uint8_t* p = a.v_packed[layer] + 3 * g;
+    const uint32_t word = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
+    TOut* out = static_cast<TOut*>(a.v_out[layer]);
+    for (int e0 = 0; e0 < 8; e0 += D) {
+      const long long v = (g * 8 + e0) / D;
+      if (v >= a.nvec) break;
+      const float sc = a.v_scales[layer][v];
+      float y[4];
+      for (int i = 0; i < D; ++i) y[i] = __fmul_rn(a.cent32[(word >> (3 * (e0 + i))) & 7u], sc);  // table[code] * scale
+      for (int h = 1; h < D; h <<= 1)
+        for (int q = 0; q < D / 2; ++q) {
+          const int i = (q / h) * 2 * h + (q % h);
+          const float lo = y[i], hi = y[i + h];
+          y[i] = __fadd_rn(lo, hi);
+          y[i + h] = __fsub_rn(lo, hi);
+        }
+      for (int i = 0; i < D; ++i) {
+        float x = __fdiv_rn(y[i], a.sqrt_d32);  // fwht.py:50 in f32
+        if (sign_bit(a.sign_bits, i)) x = -x;
+        store1(out + v * D + i, x);
+      }
+    }
+  }
+}
+
+template <typename K>
+int launch_small(K kernel, const void* args, long long work, cudaStream_t st) {
+  if (work <= 0) return PKV_OK;
+  const long long grid = std::min<long long>((work + kSmallThreads - 1) / kSmallThreads, (long long)sm_count() * 8);
+  void* params[] = {const_cast<void*>(args)};
+  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(kSmallThreads), params, 0, st) == cudaSuccess
+             ? PKV_OK
+             : PKV_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
 // canonical codes <-> packed payload
 // ---------------------------------------------------------------------------
 __global__ void unpack_kernel(const uint8_t* __restrict__ packed, long long count,
@@ -927,6 +1038,8 @@ uintptr_t packed_align(int d) {
 }  // namespace
 
 namespace {
+// head_dim 1, 2, 4: values through the thread-per-word kernels above
+bool v_small(int d) { return d < 8; }
 // PKV_CODEC_PATH=warp forces the warp-granular kernels (debug / A-B timing).
 bool stream_enabled() { return !tuning().codec_warp; }
 bool stream_fallback(int rc) { return rc == PKV_ERR_ALIGNMENT || rc == PKV_ERR_UNSUPPORTED_HEAD_DIM; }
@@ -940,7 +1053,7 @@ const char* pkv_status_string(int status) {
   switch (status) {
     case PKV_OK: return "ok";
     case PKV_ERR_INVALID_ARG: return "invalid argument";
-    case PKV_ERR_UNSUPPORTED_HEAD_DIM: return "head_dim not supported by the value kernels (8..256, power of two)";
+    case PKV_ERR_UNSUPPORTED_HEAD_DIM: return "head_dim not supported by the value kernels (1..256, power of two)";
     case PKV_ERR_CUDA: return "CUDA launch error";
     case PKV_ERR_WORKSPACE: return "workspace too small";
     case PKV_ERR_ALIGNMENT: return "misaligned pointer";
@@ -950,7 +1063,7 @@ const char* pkv_status_string(int status) {
 }
 
 int pkv_v_head_dim_supported(int d) {
-  return d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256;
+  return d == 1 || d == 2 || d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128 || d == 256;
 }
 
 size_t pkv_encode_workspace_bytes(int num_layers, int64_t num_vectors, int head_dim) {
@@ -977,6 +1090,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     return PKV_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long long nelem = (long long)num_vectors * head_dim;
+  const bool small_v = do_v && v_small(head_dim);
 
   for (int l0 = 0; l0 < num_layers; l0 += PKV_MAX_LAYERS_PER_LAUNCH) {
     const int L = std::min(num_layers - l0, (int)PKV_MAX_LAYERS_PER_LAUNCH);
@@ -1014,12 +1128,13 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
         a.v_scales[l] = v_scales ? v_scales[l0 + l] : nullptr;
         if (!a.v_in[l] || !a.v_packed[l] || !a.v_scales[l]) return PKV_ERR_INVALID_ARG;
         // the value kernels use 16 B chunk loads and word-aligned packed stores
-        if (!aligned(a.v_in[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim)) ||
-            !aligned(a.v_scales[l], 4))
+        // (the head_dim < 8 kernels load and store scalars)
+        if (!small_v && (!aligned(a.v_in[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim)) ||
+                         !aligned(a.v_scales[l], 4)))
           return PKV_ERR_ALIGNMENT;
       }
     }
-    if (stream_enabled()) {
+    if (stream_enabled() && !small_v) {
       stream::EncodeRequest q;
       std::memset(&q, 0, sizeof(q));
       q.num_layers = L;
@@ -1051,7 +1166,7 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     a.e_items = k_items;
     const bool ext_max = do_k && k_mode == PKV_K_TENSOR && k_layer_max;
     a.a_items = (do_k && k_mode == PKV_K_TENSOR && !ext_max) ? k_items : 0;
-    a.v_items = do_v ? v_items_dispatch(head_dim, num_vectors) : 0;
+    a.v_items = (do_v && !small_v) ? v_items_dispatch(head_dim, num_vectors) : 0;
     // lag: keep >= ~2 waves of warps between a layer's absmax and its key encode
     const long long round = (long long)a.a_items + a.v_items + a.e_items;
     const long long warps = (long long)sm_count() * 2 * kWarps;
@@ -1076,8 +1191,14 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
                                    cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return PKV_ERR_CUDA;
     const bool sym = do_v ? a.cb.symmetric != 0 : true;
-    const int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st, do_v, sym, sign)
-                                       : dispatch_encode<__nv_bfloat16>(a, st, do_v, sym, sign);
+    const bool tiled_v = do_v && !small_v;
+    int rc = in_dtype == PKV_F32 ? dispatch_encode<float>(a, st, tiled_v, sym, sign)
+                                 : dispatch_encode<__nv_bfloat16>(a, st, tiled_v, sym, sign);
+    if (rc == PKV_OK && small_v) {
+      const long long work = (long long)L * ((nelem + 7) / 8);
+      rc = in_dtype == PKV_F32 ? launch_small(v_encode_small_kernel<float>, &a, work, st)
+                               : launch_small(v_encode_small_kernel<__nv_bfloat16>, &a, work, st);
+    }
     if (rc != PKV_OK) return rc;
   }
   return PKV_OK;
@@ -1098,6 +1219,7 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
   if (do_v && !pkv_v_head_dim_supported(head_dim)) return PKV_ERR_UNSUPPORTED_HEAD_DIM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const long long nelem = (long long)num_vectors * head_dim;
+  const bool small_v = do_v && v_small(head_dim);
   for (int l0 = 0; l0 < num_layers; l0 += PKV_MAX_LAYERS_PER_LAUNCH) {
     const int L = std::min(num_layers - l0, (int)PKV_MAX_LAYERS_PER_LAUNCH);
     DecodeArgs a;
@@ -1131,10 +1253,11 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
         a.v_scales[l] = v_scales ? v_scales[l0 + l] : nullptr;
         a.v_out[l] = v_out[l0 + l];
         if (!a.v_packed[l] || !a.v_scales[l] || !a.v_out[l]) return PKV_ERR_INVALID_ARG;
-        if (!aligned(a.v_out[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim))) return PKV_ERR_ALIGNMENT;
+        if (!small_v && (!aligned(a.v_out[l], 16) || !aligned(a.v_packed[l], packed_align(head_dim))))
+          return PKV_ERR_ALIGNMENT;
       }
     }
-    if (stream_enabled()) {
+    if (stream_enabled() && !small_v) {
       stream::DecodeRequest q;
       std::memset(&q, 0, sizeof(q));
       q.num_layers = L;
@@ -1158,10 +1281,15 @@ int pkv_decode(int num_layers, int64_t num_vectors, int head_dim, int out_dtype,
     }
     a.vec_ok = ok ? 1 : 0;
     a.k_items = do_k ? (int)((nelem + kKElems - 1) / kKElems) : 0;
-    a.v_items = do_v ? v_items_dispatch(head_dim, num_vectors) : 0;
+    a.v_items = (do_v && !small_v) ? v_items_dispatch(head_dim, num_vectors) : 0;
     a.total_items = (long long)L * (a.k_items + a.v_items);
-    const int rc = out_dtype == PKV_F32 ? dispatch_decode<float>(a, st, do_v, sign)
-                                        : dispatch_decode<__nv_bfloat16>(a, st, do_v, sign);
+    int rc = out_dtype == PKV_F32 ? dispatch_decode<float>(a, st, do_v && !small_v, sign)
+                                  : dispatch_decode<__nv_bfloat16>(a, st, do_v && !small_v, sign);
+    if (rc == PKV_OK && small_v) {
+      const long long work = (long long)L * ((nelem + 7) / 8);
+      rc = out_dtype == PKV_F32 ? launch_small(v_decode_small_kernel<float>, &a, work, st)
+                                : launch_small(v_decode_small_kernel<__nv_bfloat16>, &a, work, st);
+    }
     if (rc != PKV_OK) return rc;
   }
   return PKV_OK;
