@@ -73,7 +73,14 @@ const char* pkv_status_string(int status);
  * re-reads them (for A/B tuning in one process). None changes a result. */
 int pkv_reload_tuning(void);
 
-/* Head dims supported by the value kernels: 8, 16, 32, 64, 128, 256.
+/* The last failing CUDA runtime / driver call of the CALLING HOST THREAD,
+ * as "<call>: <error name> (<error string>)", or "" if none failed. Set
+ * whenever an entry point returns PKV_ERR_CUDA; not cleared by later
+ * successful calls. (No reference counterpart: the reference is CPU numpy.) */
+const char* pkv_last_cuda_error(void);
+
+/* Head dims supported by the value kernels: 1, 2, 4 (thread-per-word exact
+ * kernels), 8 .. 256 (tiled kernels; 64 and 128 streamed through TMA).
  * Key kernels accept any head_dim. Returns 1 if supported. */
 int pkv_v_head_dim_supported(int head_dim);
 

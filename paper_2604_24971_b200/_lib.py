@@ -15,6 +15,7 @@ from pathlib import Path
 from ._build import LIB_PATH
 
 PKV_OK = 0
+PKV_ERR_CUDA = -3
 PKV_F32 = 0
 PKV_BF16 = 1
 PKV_K_TENSOR = 0
@@ -40,6 +41,7 @@ SIGNATURES: dict[str, tuple] = {
     "pkv_abi_version": (c_int, []),
     "pkv_status_string": (ctypes.c_char_p, [c_int]),
     "pkv_reload_tuning": (c_int, []),
+    "pkv_last_cuda_error": (ctypes.c_char_p, []),
     "pkv_v_head_dim_supported": (c_int, [c_int]),
     "pkv_encode_workspace_bytes": (c_size, [c_int, c_i64, c_int]),
     "pkv_encode": (
@@ -114,7 +116,10 @@ def reload_tuning() -> None:
 
 def check(status: int, what: str) -> None:
     if status != PKV_OK:
-        msg = load().pkv_status_string(status).decode()
+        lib = load()
+        msg = lib.pkv_status_string(status).decode()
+        if status == PKV_ERR_CUDA:
+            msg += f" [{lib.pkv_last_cuda_error().decode()}]"
         raise LibraryError(f"{what} failed: {msg} (status {status})")
 
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "pkv_common.cuh"
 
 namespace pkv {
@@ -84,7 +85,7 @@ extern "C" int pkv_k_absmax(int num_layers, int64_t count, int in_dtype, const v
   if (in_dtype != PKV_F32 && in_dtype != PKV_BF16) return PKV_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (num_layers == 0) return PKV_OK;
-  if (cudaMemsetAsync(max_bits, 0, sizeof(uint32_t) * num_layers, st) != cudaSuccess) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaMemsetAsync(max_bits, 0, sizeof(uint32_t) * num_layers, st), "cudaMemsetAsync")) return PKV_ERR_CUDA;
   if (count == 0) return PKV_OK;
   const int eb = in_dtype == PKV_F32 ? 4 : 2;
   int sms = 148;
@@ -107,7 +108,7 @@ extern "C" int pkv_k_absmax(int num_layers, int64_t count, int in_dtype, const v
     const long long want = (units + 4LL * kAbsThreads - 1) / (4LL * kAbsThreads);
     const int per_layer = (int)std::max(1LL, std::min(want, (long long)std::max(1, 4 * sms / L)));
     absmax_kernel<<<dim3(per_layer, L), kAbsThreads, 0, st>>>(a);
-    if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
+    if (!pkv::cuda_ok(cudaGetLastError(), "kernel launch")) return PKV_ERR_CUDA;
   }
   return PKV_OK;
 }

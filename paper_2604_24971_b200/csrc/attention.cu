@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "pkv_common.cuh"
 #include "tuning.h"
 
@@ -927,27 +928,28 @@ inline int attn_splits(int kv_heads, long long T, int rows, int head_dim) {
 template <int D, int RTILE>
 int launch_rt(Args& a, cudaStream_t st) {
   using AT = AttnTile<D, RTILE>;
-  if (cudaFuncSetAttribute(prefix_kernel2<D, RTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)AT::SMEM) != cudaSuccess)
+  if (!pkv::cuda_ok(cudaFuncSetAttribute(prefix_kernel2<D, RTILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)AT::SMEM),
+                    "cudaFuncSetAttribute"))
     return PKV_ERR_CUDA;
   const int row_tiles = (a.rows + RTILE - 1) / RTILE;
   dim3 grid(a.splits, a.kv_heads, row_tiles);
   prefix_kernel2<D, RTILE><<<grid, kAttnThreads2, AT::SMEM, st>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaGetLastError(), "kernel launch")) return PKV_ERR_CUDA;
   combine_kernel<D><<<a.rows * a.kv_heads, 32 * kCombineWarps, 0, st>>>(a);
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(cudaGetLastError(), "kernel launch") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D, int WR>
 int launch_mma(Args& a, cudaStream_t st) {
   using MT = mma::MmaTile<D, WR>;
-  if (cudaFuncSetAttribute(prefix_mma<D, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MT::SMEM) !=
-      cudaSuccess)
+  if (!pkv::cuda_ok(cudaFuncSetAttribute(prefix_mma<D, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, MT::SMEM),
+                    "cudaFuncSetAttribute"))
     return PKV_ERR_CUDA;
   const int row_tiles = (a.rows + MT::RT - 1) / MT::RT;
   dim3 grid(a.splits, a.kv_heads, row_tiles);
   prefix_mma<D, WR><<<grid, 128, MT::SMEM, st>>>(a);
-  if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaGetLastError(), "kernel launch")) return PKV_ERR_CUDA;
   // combine as a programmatic dependent launch (PDL): it may start launching
   // before the prefix grid ends and waits on griddepcontrol.wait
   cudaLaunchConfig_t cfg = {};
@@ -960,8 +962,8 @@ int launch_mma(Args& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, combine_kernel<D>, a) != cudaSuccess) return PKV_ERR_CUDA;
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaLaunchKernelEx(&cfg, combine_kernel<D>, a), "cudaLaunchKernelEx")) return PKV_ERR_CUDA;
+  return pkv::cuda_ok(cudaGetLastError(), "kernel launch") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D>

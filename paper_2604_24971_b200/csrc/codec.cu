@@ -32,6 +32,7 @@
 #include <cstring>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "pkv_common.cuh"
 #include "codec_common.cuh"
 #include "stream_codec.h"
@@ -858,7 +859,8 @@ int launch_small(K kernel, const void* args, long long work, cudaStream_t st) {
   if (work <= 0) return PKV_OK;
   const long long grid = std::min<long long>((work + kSmallThreads - 1) / kSmallThreads, (long long)sm_count() * 8);
   void* params[] = {const_cast<void*>(args)};
-  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(kSmallThreads), params, 0, st) == cudaSuccess
+  return pkv::cuda_ok(cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(kSmallThreads), params, 0, st),
+                      "cudaLaunchKernel")
              ? PKV_OK
              : PKV_ERR_CUDA;
 }
@@ -960,7 +962,7 @@ int launch_encode(EncodeArgs& a, cudaStream_t st) {
   void* params[] = {(void*)&a};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)grid), dim3(kThreads),
                                                     params, 0, st);
-  return e == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(e, "cudaLaunchCooperativeKernel") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D, typename TIn>
@@ -990,7 +992,7 @@ int launch_decode(DecodeArgs& a, cudaStream_t st) {
   if (grid > need) grid = need;
   if (grid < 1) return PKV_OK;
   fn<<<(unsigned)grid, kThreads, 0, st>>>(a);
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(cudaGetLastError(), "kernel launch") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D, typename TOut>
@@ -1184,11 +1186,12 @@ int pkv_encode(int num_layers, int64_t num_vectors, int head_dim, int in_dtype,
     }
     a.round_start[a.num_rounds] = acc;
     a.total_items = acc;
-    if (cudaMemsetAsync(workspace, 0, (size_t)(2 * L + 2) * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
+    if (!pkv::cuda_ok(cudaMemsetAsync(workspace, 0, (size_t)(2 * L + 2) * sizeof(uint32_t), st), "cudaMemsetAsync")) return PKV_ERR_CUDA;
     // external per-layer maxima: the key encode reads them where the absmax
     // items would have left theirs (and, with a_items == 0, never waits)
-    if (ext_max && cudaMemcpyAsync(workspace, k_layer_max + l0, (size_t)L * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    if (ext_max && !pkv::cuda_ok(cudaMemcpyAsync(workspace, k_layer_max + l0, (size_t)L * sizeof(uint32_t),
+                                                 cudaMemcpyDeviceToDevice, st),
+                                 "cudaMemcpyAsync"))
       return PKV_ERR_CUDA;
     const bool sym = do_v ? a.cb.symmetric != 0 : true;
     const bool tiled_v = do_v && !small_v;
@@ -1301,7 +1304,7 @@ int pkv_unpack_codes(const uint8_t* packed, int64_t count, uint8_t* codes, void*
   const long long groups = (count + 7) / 8;
   const int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
   unpack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(packed, count, codes);
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(cudaGetLastError(), "kernel launch") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 int pkv_pack_codes(const uint8_t* codes, int64_t count, uint8_t* packed, uint32_t* bad_code,
@@ -1311,7 +1314,7 @@ int pkv_pack_codes(const uint8_t* codes, int64_t count, uint8_t* packed, uint32_
   const long long groups = (count + 7) / 8;
   const int grid = (int)std::min<long long>((groups + 255) / 256, 148LL * 16);
   pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(codes, count, packed, bad_code);
-  return cudaGetLastError() == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(cudaGetLastError(), "kernel launch") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 int64_t pkv_selftest(int what, void* scratch, size_t scratch_bytes, void* stream) {
@@ -1319,14 +1322,14 @@ int64_t pkv_selftest(int what, void* scratch, size_t scratch_bytes, void* stream
   if (!scratch || scratch_bytes < 4 * sizeof(uint32_t)) return PKV_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint32_t* cnt = static_cast<uint32_t*>(scratch);
-  if (cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), st) != cudaSuccess) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaMemsetAsync(cnt, 0, 4 * sizeof(uint32_t), st), "cudaMemsetAsync")) return PKV_ERR_CUDA;
   selftest_div_kernel<8><<<1024, 256, 0, st>>>(cnt + 0);
   selftest_div_kernel<32><<<1024, 256, 0, st>>>(cnt + 1);
   selftest_div_kernel<128><<<1024, 256, 0, st>>>(cnt + 2);
   selftest_div127_kernel<<<1024, 256, 0, st>>>(cnt + 3);
   uint32_t host[4] = {0, 0, 0, 0};
-  if (cudaMemcpyAsync(host, cnt, sizeof(host), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PKV_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaMemcpyAsync(host, cnt, sizeof(host), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync")) return PKV_ERR_CUDA;
+  if (!pkv::cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize")) return PKV_ERR_CUDA;
   return (int64_t)host[0] + host[1] + host[2] + host[3];
 }
 

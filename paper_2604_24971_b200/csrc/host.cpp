@@ -7,11 +7,13 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "tuning.h"
 
 namespace pkv {
@@ -52,6 +54,25 @@ void reload_tuning() {
 extern "C" int pkv_reload_tuning(void) {
   pkv::reload_tuning();
   return PKV_OK;
+}
+
+namespace pkv {
+CudaFailure& last_cuda_failure() {
+  static thread_local CudaFailure f;
+  return f;
+}
+}  // namespace pkv
+
+extern "C" const char* pkv_last_cuda_error(void) {
+  static thread_local char buf[256];
+  const pkv::CudaFailure& f = pkv::last_cuda_failure();
+  if (f.err == 0) return "";
+  if (f.driver)
+    std::snprintf(buf, sizeof(buf), "%s: CUresult %d", f.what, f.err);
+  else
+    std::snprintf(buf, sizeof(buf), "%s: %s (%s)", f.what, cudaGetErrorName((cudaError_t)f.err),
+                  cudaGetErrorString((cudaError_t)f.err));
+  return buf;
 }
 
 namespace {

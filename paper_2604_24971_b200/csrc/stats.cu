@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "pkv_common.cuh"
 
 namespace pkv {
@@ -152,12 +153,12 @@ extern "C" int pkv_layer_stats(int num_layers, int64_t count, int in_dtype, cons
         if (reinterpret_cast<uintptr_t>(p) % 16) a.vec = 0;
     }
     if (count == 0) {
-      if (cudaMemsetAsync(a.out, 0, sizeof(double) * 4 * L, st) != cudaSuccess) return PKV_ERR_CUDA;
+      if (!pkv::cuda_ok(cudaMemsetAsync(a.out, 0, sizeof(double) * 4 * L, st), "cudaMemsetAsync")) return PKV_ERR_CUDA;
       continue;
     }
     stats_partial<<<dim3(a.blocks, L), kStatThreads, 0, st>>>(a);
     stats_final<<<L, 32, 0, st>>>(a);
-    if (cudaGetLastError() != cudaSuccess) return PKV_ERR_CUDA;
+    if (!pkv::cuda_ok(cudaGetLastError(), "kernel launch")) return PKV_ERR_CUDA;
   }
   return PKV_OK;
 }

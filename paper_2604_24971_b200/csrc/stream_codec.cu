@@ -30,6 +30,7 @@
 #include <mutex>
 
 #include "../../include/polykv.h"
+#include "diag.h"
 #include "codec_common.cuh"
 #include "pkv_common.cuh"
 #include "tma.cuh"
@@ -1808,11 +1809,30 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled is a driver call and needs a current context. A
+// host thread that has made no context-binding runtime call yet (a fresh
+// Python thread reading the pool) has none: CUDA_ERROR_INVALID_CONTEXT.
+// cudaFree(nullptr) binds the current device's primary context, once per
+// thread and device.
+bool bind_context() {
+  static thread_local int bound = -1;
+  int dev = 0;
+  if (!pkv::cuda_ok(cudaGetDevice(&dev), "cudaGetDevice")) return false;
+  if (bound == dev) return true;
+  if (!pkv::cuda_ok(cudaFree(nullptr), "cudaFree(nullptr) (bind the primary context)")) return false;
+  bound = dev;
+  return true;
+}
+
 // [nvec, D] head-vector tensor of one layer as a 2-D TMA map with the box
 // geometry of Tile<D, eb>.
 bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec, int chunk) {
+  if (!bind_context()) return false;
   auto fn = encode_fn();
-  if (!fn) return false;
+  if (!fn) {
+    pkv::driver_fail(-1, "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    return false;
+  }
   const int RB = D * eb, IB = RB < 128 ? RB : 128, VR = chunk / D, BR = VR / ((VR + 255) / 256);  // == Tile::BR
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)nvec};
   cuuint64_t strides[1] = {(cuuint64_t)RB};
@@ -1825,22 +1845,29 @@ bool make_map(CUtensorMap* m, const void* base, int eb, int D, long long nvec, i
   const CUresult r = fn(m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) pkv::driver_fail((int)r, "cuTensorMapEncodeTiled");
   return r == CUDA_SUCCESS;
 }
 
 template <typename K>
 int coop_launch(K kernel, const void* args, size_t smem, int threads, cudaStream_t st) {
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (!pkv::cuda_ok(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "cudaFuncSetAttribute"))
     return PKV_ERR_CUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+  if (!pkv::cuda_ok(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
+                    "cudaOccupancyMaxActiveBlocksPerMultiprocessor"))
     return PKV_ERR_CUDA;
+  if (per_sm < 1) {
+    pkv::cuda_ok(cudaErrorInvalidConfiguration, "occupancy: the kernel does not fit an SM");
+    return PKV_ERR_CUDA;
+  }
   void* params[] = {const_cast<void*>(args)};
   const cudaError_t e =
       // one persistent CTA per SM (the role split and static slices assume it)
       cudaLaunchCooperativeKernel((const void*)kernel, dim3((unsigned)sm_count()), dim3(threads), params,
                                   smem, st);
-  return e == cudaSuccess ? PKV_OK : PKV_ERR_CUDA;
+  return pkv::cuda_ok(e, "cudaLaunchCooperativeKernel") ? PKV_OK : PKV_ERR_CUDA;
 }
 
 template <int D, typename TIn>
@@ -1984,7 +2011,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       else if (!make_map(&a->tm_v[l], a->v_in[l], eb, r.head_dim, r.num_vectors, kEncChunk)) rc = PKV_ERR_CUDA;
     }
   }
-  if (rc == PKV_OK && cudaMemsetAsync(r.ws, 0, ws_need, st) != cudaSuccess) rc = PKV_ERR_CUDA;
+  if (rc == PKV_OK && !pkv::cuda_ok(cudaMemsetAsync(r.ws, 0, ws_need, st), "cudaMemsetAsync")) rc = PKV_ERR_CUDA;
   // One launch; the grid is split by role so every SM runs a single code
   // path (mixing the key and value paths on one SM thrashes its instruction
   // cache): value CTAs are ALU-bound, key CTAs (absmax pass, key barrier,

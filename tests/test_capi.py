@@ -47,6 +47,7 @@ def test_abi_and_status(lib):
     assert lib.pkv_abi_version() == 4
     assert lib.pkv_status_string(0) == b"ok"
     assert b"head_dim" in lib.pkv_status_string(-2)
+    assert lib.pkv_last_cuda_error() == b""  # no CUDA call has failed on this thread
     assert lib.pkv_v_head_dim_supported(128) == 1 and lib.pkv_v_head_dim_supported(4) == 1
     assert lib.pkv_v_head_dim_supported(512) == 0 and lib.pkv_v_head_dim_supported(12) == 0
     # per layer: u32 max + u32 published-CTA count (+16); the warp path needs 2L+2 words
