@@ -1249,6 +1249,10 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
           constexpr int kEncChunk = enc_chunk<TIn>();
           const long long e0 = (long long)it.idx * kEncChunk;
           const uint32_t bytes = (uint32_t)(min((long long)kEncChunk, a.nelem - e0) * (long long)sizeof(TIn));
+          if (a.dbg == 5 && it.kind == kKeyEnc) {  // timing experiment: no L2 re-read (wrong codes)
+            tma::mbar_arrive(bar);
+            return;
+          }
           tma::mbar_arrive_expect_tx(bar, bytes);
           tma::bulk_g2s(dst, static_cast<const TIn*>(a.k_in[it.layer]) + e0, bytes, bar,
                         it.kind == kAbsmax ? pol_last : pol_first);
