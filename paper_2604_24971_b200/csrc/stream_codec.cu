@@ -140,7 +140,7 @@ struct EncArgs {
   int num_layers, head_dim, k_mode, in_bytes;
   long long nvec, nelem;
   int nE, nV;  // items per layer
-  int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys, 4 no layer wait
+  int dbg;  // PKV_DBG_ENC experiments: 1 skip all math, 2 skip values, 3 skip keys, 4 no layer wait, 5 no key re-read
   unsigned int total;
   float delta;
   Codebook3 cb;
@@ -152,6 +152,10 @@ struct EncArgs {
   const uint32_t* k_max_ext;  // per-tensor keys: external max|K| bits per layer (no absmax pass)
   int value_ctas;             // CTAs [0, value_ctas) encode values, the rest keys
   int nA;                     // absmax items per layer (per-tensor mode)
+  int abs_G;                  // > 0: CTAs issuing absmax items (round-robin, layer-major); each
+                              // publishes its layer max once, after its last item of the layer.
+                              // 0: every item publishes (static key schedule)
+  int abs_target;             // layer_done[l] value meaning "layer l's max is complete"
   int nseg;                   // key-role segments of nE items: kind (A/E) + layer
   int key_lag;                // absmax layers allowed ahead of the key encode
   int abs_lead;               // > 0: the VALUE CTAs run the absmax items, abs_lead layers ahead of their V cursor
@@ -1107,7 +1111,39 @@ struct alignas(8) Ctl {
   // can start the next use of the stage while a slow one still folds this one
   uint32_t gmax[kMaxGroups][kMaxSG][2];
   uint32_t gcnt[kMaxGroups][kMaxSG][2];
+  // encode: this CTA's per-layer absmax fold (max bits, items folded)
+  uint32_t cta_max[kMaxL];
+  uint32_t cta_cnt[kMaxL];
 };
+
+// Items t in [0, x) with t = r (mod G).
+__device__ __forceinline__ uint32_t residues_below(uint32_t x, uint32_t r, uint32_t G) {
+  return x > r ? (x - 1 - r) / G + 1 : 0u;
+}
+
+// One absmax item's max (already folded over the group's warps) into the
+// layer maximum. With abs_G > 0 it is folded into the CTA's per-layer slot and
+// the CTA's LAST item of the layer publishes: one global atomicMax and one
+// release per CTA and layer instead of per item (a release waits for all of
+// the thread's earlier global stores -- the key codes it wrote -- so one per
+// item stalled the key role: C3 f32 encode 318 -> 305 us without them).
+__device__ __forceinline__ void fold_absmax(const EncArgs& a, Ctl* ctl, int l, uint32_t m, uint32_t rank) {
+  if (a.abs_G <= 0) {
+    if (m) atomicMax(a.layer_max + l, m);
+    red_release_add(a.layer_done + l, 1u);  // orders the max before the count
+    return;
+  }
+  if (m) atomicMax(&ctl->cta_max[l], m);
+  __threadfence_block();
+  const uint32_t G = (uint32_t)a.abs_G, lo = (uint32_t)l * (uint32_t)a.nA, hi = lo + (uint32_t)a.nA;
+  const uint32_t mine = residues_below(hi, rank, G) - residues_below(lo, rank, G);
+  if (atomicAdd(&ctl->cta_cnt[l], 1u) + 1u == mine) {
+    __threadfence_block();
+    const uint32_t cm = atomicOr(&ctl->cta_max[l], 0u);
+    if (cm) atomicMax(a.layer_max + l, cm);
+    red_release_add(a.layer_done + l, 1u);
+  }
+}
 
 template <int D, typename TIn>
 constexpr size_t enc_smem_bytes() {
@@ -1211,7 +1247,11 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
       }
     tma::fence_mbar_init();
   }
-  if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxL) {
+    ctl->ready[threadIdx.x] = 0;
+    ctl->cta_max[threadIdx.x] = 0;
+    ctl->cta_cnt[threadIdx.x] = 0;
+  }
   if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
   if (threadIdx.x < kMaxGroups * kMaxSG * 2) {
     (&ctl->gmax[0][0][0])[threadIdx.x] = 0;
@@ -1355,7 +1395,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
               stage(el, pending_max);
               continue;
             }
-            if (polled == el && polled_cnt >= nA) {
+            if (polled == el && polled_cnt >= (uint32_t)a.abs_target) {
               request_max(el);
             } else {
               polled = el;
@@ -1370,7 +1410,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
             if (pending != el) {  // nothing else to issue: wait for layer el's absmax items
               uint32_t spins = 0;
               uint64_t t0 = 0;
-              while (ld_relaxed_u32(a.layer_done + el) < nA) {
+              while (ld_relaxed_u32(a.layer_done + el) < (uint32_t)a.abs_target) {
                 __nanosleep(128);
                 tma::watchdog(spins, t0);
               }
@@ -1386,6 +1426,8 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
   }
 
   // ---------------- consumers (warps work independently) ----------------
+  // rank of this CTA among the CTAs that issue absmax items
+  const uint32_t abs_rank = a.abs_lead > 0 ? (uint32_t)pos : (uint32_t)pos - (uint32_t)a.value_ctas;
   const int g = (warp - 1) / kWarpsPerGroup;
   const int wig = (warp - 1) % kWarpsPerGroup;
   const int gt = threadIdx.x - 32 - g * kGroupThreads;
@@ -1415,8 +1457,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         if (atomicAdd(&ctl->gcnt[g][k][par], 1u) == kWarpsPerGroup - 1) {
           const uint32_t gm = atomicExch(&ctl->gmax[g][k][par], 0u);
           ctl->gcnt[g][k][par] = 0;
-          if (gm) atomicMax(a.layer_max + it.layer, gm);
-          red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
+          fold_absmax(a, ctl, it.layer, gm, abs_rank);
         }
       }
     } else if (skip) {
@@ -1425,7 +1466,7 @@ __global__ void __launch_bounds__(kEncThreads, 1) enc_kernel(const __grid_consta
         if (lane == 0 && !*reinterpret_cast<volatile const uint32_t*>(&ctl->ready[it.layer])) {
           uint32_t spins = 0;
           uint64_t t0 = 0;
-          while (ld_acquire_u32(a.layer_done + it.layer) < (uint32_t)a.nA) {
+          while (ld_acquire_u32(a.layer_done + it.layer) < (uint32_t)a.abs_target) {
             __nanosleep(64);
             tma::watchdog(spins, t0);
           }
@@ -1494,7 +1535,11 @@ __global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_cons
       }
     tma::fence_mbar_init();
   }
-  if (threadIdx.x < kMaxL) ctl->ready[threadIdx.x] = 0;
+  if (threadIdx.x < kMaxL) {
+    ctl->ready[threadIdx.x] = 0;
+    ctl->cta_max[threadIdx.x] = 0;
+    ctl->cta_cnt[threadIdx.x] = 0;
+  }
   if (a.k_max_ext && threadIdx.x < a.num_layers) ctl->layer_max[threadIdx.x] = a.k_max_ext[threadIdx.x];
   if (threadIdx.x < kMaxGroups * kMaxSG * 2) {
     (&ctl->gmax[0][0][0])[threadIdx.x] = 0;
@@ -1560,7 +1605,7 @@ __global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_cons
             ready = el;
             continue;
           }
-          if (polled == el && polled_cnt >= nA) {
+          if (polled == el && polled_cnt >= (uint32_t)a.abs_target) {
             fence_acq_rel_gpu();
             pending_max = ld_relaxed_u32(a.layer_max + el);  // staged at the next call
             pending = el;
@@ -1653,8 +1698,7 @@ __global__ void __launch_bounds__(kCoThreads, 1) enc_co_kernel(const __grid_cons
         if (atomicAdd(&ctl->gcnt[g][k][par], 1u) == kCoWPG - 1) {
           const uint32_t gm = atomicExch(&ctl->gmax[g][k][par], 0u);
           ctl->gcnt[g][k][par] = 0;
-          if (gm) atomicMax(a.layer_max + it.layer, gm);
-          red_release_add(a.layer_done + it.layer, 1u);  // orders the max before the count
+          fold_absmax(a, ctl, it.layer, gm, blockIdx.x);
         }
       }
     } else if (it.kind == kKeyEnc) {
@@ -2064,7 +2108,12 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // (round 2, after the key fast-path change: C3 bf16 0.34 -> 253 us, 0.38 -> 261,
       // 0.42 -> 275; C3 f32 0.38 -> 365 us, 0.42 -> 335, 0.45 -> 327, 0.49 -> 350)
       const bool d128 = r.head_dim >= 128;
-      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.45 : 0.34) : 0.42) : (d128 ? 0.43 : 0.46);
+      // (per-CTA absmax publication, C3 f32: 56 key CTAs 324 us, 58 316, 60 308, 62 301.5, 64 306,
+      // 66 315; bf16: 46 246, 48 237, 50 235, 52 240 -- profiles/r02/frac3.txt)
+      // (C2, d64: f32 0.42 -> 220 us, 0.459 -> 198, 0.486 -> 190, 0.514 -> 197; bf16 0.338 -> 157,
+      // 0.365 -> 147.5, 0.392 -> 152 -- frac_c2*.txt)
+      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.419 : 0.34) : (eb == 4 ? 0.486 : 0.365))
+                                             : (d128 ? 0.43 : 0.46);
       if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
       // an even count: the two SMs of a TPC must run the same role (an odd
@@ -2075,6 +2124,19 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       key_ctas = grid;
     }
     a->value_ctas = grid - key_ctas;
+    // which CTAs issue the absmax items (round-robin over the layer-major
+    // list), and the layer_done count that completes a layer's max: one
+    // publication per contributing CTA (fold_absmax), or per item for the
+    // static key schedule
+    a->abs_G = 0;
+    a->abs_target = a->nA;
+    if (a->nA) {
+      const int G = co ? grid : a->abs_lead > 0 ? a->value_ctas : kKeyDynamic ? key_ctas : 0;
+      if (G > 0) {
+        a->abs_G = G;
+        a->abs_target = std::min(G, a->nA);
+      }
+    }
     if (co) {
       a->co_roles = (do_k && do_v) ? 0 : (do_v ? 1 : 2);
       a->value_ctas = grid;

@@ -212,6 +212,14 @@ def raise_for_status(status: torch.Tensor) -> None:
         raise CorruptBlockError("corrupt block: code out of range for 3-bit codebook")
 
 
+def _rows(t: torch.Tensor, idx: list) -> torch.Tensor:
+    """t[idx] without a host index tensor when idx is a contiguous range (so the
+    call stays CUDA-graph capturable)."""
+    if idx == list(range(idx[0], idx[0] + len(idx))):
+        return t[idx[0]:idx[0] + len(idx)].contiguous()
+    return t[torch.tensor(idx, device=t.device)].contiguous()
+
+
 def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, sign_seed,
                    k_scale_mode: str, *, device=None, check: bool = True, arena: _Arena | None = None,
                    k_layer_max: torch.Tensor | None = None):
@@ -269,8 +277,8 @@ def _encode_layers(ks, vs, geometry: ModelGeometry, codebook: Codebook | None, s
                 v_scales=[a.v_scales[i, :g.vectors_per_tensor] for i in vg] if vg else None,
                 centroids=(codebook.centroids if codebook is not None else np.zeros(8)),
                 sign_seed=sign_seed, status=status, replay=a.replay, device=device,
-                k_layer_max=(k_layer_max[kg].contiguous() if (k_layer_max is not None and kg
-                                                              and k_scale_mode == "tensor") else None))
+                k_layer_max=(_rows(k_layer_max, kg) if (k_layer_max is not None and kg
+                                                         and k_scale_mode == "tensor") else None))
             if not contiguous:
                 for j, i in enumerate(layers):
                     a.status[i] |= status[j]
