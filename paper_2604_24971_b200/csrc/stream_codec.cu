@@ -626,6 +626,13 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
 // ---------------------------------------------------------------------------
 // encode: key items
 // ---------------------------------------------------------------------------
+// max(|a|, |b|) with the sign of a ^ b, NaN if either input is NaN
+__device__ __forceinline__ float absmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.xorsign.abs.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // |x| bit patterns of 8 inputs from shared memory, max-reduced
 template <typename TIn>
 __device__ __forceinline__ uint32_t lds_absmax8(uint32_t a);
@@ -666,6 +673,27 @@ __device__ uint32_t enc_absmax_item(const EncArgs& a, const Item& it, uint32_t i
       }
       const uint32_t ab = *reinterpret_cast<uint32_t*>(&acc);
       m = max(ab & 0x7fffu, (ab >> 16) & 0x7fffu) << 16;  // |.| patterns: NaN (0x7fff) > inf
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      return m;
+    }
+  }
+  if constexpr (sizeof(TIn) == 4) {
+    if (n == kEncChunk) {
+      // f32: one NaN-propagating max of magnitudes per element
+      // (max.NaN.xorsign.abs: |result| = max(|a|, |b|), NaN if either is NaN;
+      // the sign is dropped at the end), two independent chains
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < kEncChunk / 8 / kGroupThreads; ++i) {
+        const uint32_t a0 = in_s + (i * kGroupThreads + gt) * 32;
+        const uint4 w = tma::lds128(a0), v = tma::lds128(a0 + 16);
+        acc0 = absmax_nan(absmax_nan(acc0, __uint_as_float(w.x)), __uint_as_float(w.y));
+        acc1 = absmax_nan(absmax_nan(acc1, __uint_as_float(w.z)), __uint_as_float(w.w));
+        acc0 = absmax_nan(absmax_nan(acc0, __uint_as_float(v.x)), __uint_as_float(v.y));
+        acc1 = absmax_nan(absmax_nan(acc1, __uint_as_float(v.z)), __uint_as_float(v.w));
+      }
+      m = __float_as_uint(absmax_nan(acc0, acc1)) & 0x7fffffffu;  // NaN (0x7fc00000) > inf like the bit path
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
       return m;

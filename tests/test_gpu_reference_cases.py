@@ -392,3 +392,19 @@ def test_small_head_dim_pool_reads_like_the_oracle(d):
             k, v = view.get_kv_for_layer(i)
             assert np.array_equal(k.numpy().view(np.uint32), kw.view(np.uint32))
             assert np.array_equal(v.numpy().view(np.uint32), vw.view(np.uint32))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("bad", [float("nan"), float("-inf"), -float("nan")])
+def test_nonfinite_key_in_a_full_item_raises(dtype, bad):
+    # model.py rejects NaN/Inf (GeometryError); on the device the key absmax
+    # of a FULL streamed item (16384 elements here, two f32 / one bf16 item)
+    # must carry a NaN or an infinity into the layer maximum
+    g = pk.ModelGeometry(num_layers=2, kv_heads=2, head_dim=128, seq_len=64)
+    dump = pk.synth_gaussian_dump(g, seed=3, device="cuda", dtype=dtype)
+    dump.layers[1][0].values[0, 1, 40, 77] = bad
+    with pytest.raises(pk.GeometryError, match="NaN or Inf"):
+        pk.build_pool(dump)
+    k = dump.layers[1][0]
+    with pytest.raises(pk.GeometryError, match="NaN or Inf"):
+        pk.quantize_k(k)
