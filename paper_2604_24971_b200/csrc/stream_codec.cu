@@ -226,35 +226,27 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, f2(-1.f, -1.f), a); }
 
 // ---------------------------------------------------------------------------
-// Sylvester FWHT over N contiguous coordinates held as N/2 f32 pairs:
-//   xp[(c >> 1) * 8 + e] = (x[8c + e], x[8c + 8 + e])   for even c.
+// Sylvester FWHT over N contiguous coordinates held as N/2 f32 pairs of
+// neighbours:  xp[q] = (x[2q], x[2q + 1]).
 // Stages run half = 1, 2, 4, ..., N/2 with lo' = lo + hi, hi' = lo - hi,
 // exactly kvpool/fwht.py:31-39, so every output is bit-identical to numpy.
+// half = 1 combines the two halves of one register pair (two scalar ops);
+// every later stage combines whole pairs (paired FADD2 / FFMA2). The layout
+// is the one 16-byte loads and table lookups produce, so filling it needs no
+// register moves (the previous (x[8c+e], x[8c+8+e]) pairing cost ~1.8
+// IMAD.MOV per coordinate in the encode).
 // ---------------------------------------------------------------------------
 template <int N>
 __device__ __forceinline__ void fwht_pairs(float2* xp) {
   constexpr int NP = N / 2;
 #pragma unroll
-  for (int h = 1; h < 8; h <<= 1) {  // coordinate bits 0..2
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      if (p & h) continue;
-      const float2 a = xp[p], b = xp[p + h];
-      xp[p] = add2(a, b);
-      xp[p + h] = sub2(a, b);
-    }
-  }
-  // coordinate bit 3: inside each pair, (x, y) -> (x + y, x - y). Two scalar
-  // ops: a paired FFMA2 would need a (1, -1) register pair per use.
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
+  for (int p = 0; p < NP; ++p) {  // coordinate bit 0
     const float a = xp[p].x, b = xp[p].y;
-    xp[p].x = a + b;
-    xp[p].y = a - b;
+    xp[p].x = __fadd_rn(a, b);
+    xp[p].y = __fsub_rn(a, b);
   }
-  // coordinate bits 4.. : pair-index bits 3..
 #pragma unroll
-  for (int h = 8; h < NP; h <<= 1) {
+  for (int h = 1; h < NP; h <<= 1) {  // coordinate bits 1.. = pair-index bits 0..
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       if (p & h) continue;
@@ -285,7 +277,7 @@ __device__ __forceinline__ void fwht_vector(float2* xp, int s) {
 }
 
 // coordinate (within the lane's CPT) of pair p, half hh
-__device__ __forceinline__ constexpr int coord_of(int p, int hh) { return ((p >> 3) * 2 + hh) * 8 + (p & 7); }
+__device__ __forceinline__ constexpr int coord_of(int p, int hh) { return 2 * p + hh; }
 
 template <int NP>
 __device__ __forceinline__ void apply_sign(float2* xp, const uint32_t* bits, int base) {
@@ -482,10 +474,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         lds_chunk8<TIn>(in_s + TL::off(vr, 2 * gc), in_s + TL::off(vr, 2 * gc + 1), t);
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (c & 1) xp[(c >> 1) * 8 + e].y = t[e];
-        else xp[(c >> 1) * 8 + e].x = t[e];
-      }
+      for (int i = 0; i < 4; ++i) xp[4 * c + i] = f2(t[2 * i], t[2 * i + 1]);
     }
     // squared norm in fp64 from the inputs (the rotation is orthogonal);
     // every x^2 is exact in fp64 and the sum is good to ~D * 2^-53.
@@ -536,7 +525,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
       // complemented once at the end.
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        const int p = (q & ~7) | (7 - (q & 7));  // e = 7 .. 0 within each chunk pair
+        const int p = (q & ~3) | (3 - (q & 3));  // pairs (7,6), (5,4), .. of each chunk
         const float2 u = xp[p];
         const float2 au = f2(fabsf(u.x), fabsf(u.y));
         const float2 d1 = __fadd2_rn(au, T1), d2 = __fadd2_rn(au, T2), d3 = __fadd2_rn(au, T3);
@@ -546,13 +535,14 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         gb = fminf(gb, fminf(fabsf(d2.x), fabsf(d2.y)));
         ga = fminf(ga, fminf(fabsf(d3.x), fabsf(d3.y)));
         gb = fminf(gb, fminf(au.x, au.y));
-        const int c0 = (p >> 3) * 2;
+        const int c = p >> 2;
         const uint32_t ux = __float_as_uint(u.x), uy = __float_as_uint(u.y);
         const uint32_t b1x = __float_as_uint(d2.x) ^ ux, b1y = __float_as_uint(d2.y) ^ uy;
         const uint32_t b0x = __float_as_uint(d1.x) ^ __float_as_uint(d3.x) ^ b1x;
         const uint32_t b0y = __float_as_uint(d1.y) ^ __float_as_uint(d3.y) ^ b1y;
-        words[c0] = __funnelshift_l(b0x, __funnelshift_l(b1x, __funnelshift_l(ux, words[c0], 1), 1), 1);
-        words[c0 + 1] = __funnelshift_l(b0y, __funnelshift_l(b1y, __funnelshift_l(uy, words[c0 + 1], 1), 1), 1);
+        // y is the odd (higher) coordinate of the pair: its bits go in first
+        words[c] = __funnelshift_l(b0y, __funnelshift_l(b1y, __funnelshift_l(uy, words[c], 1), 1), 1);
+        words[c] = __funnelshift_l(b0x, __funnelshift_l(b1x, __funnelshift_l(ux, words[c], 1), 1), 1);
       }
 #pragma unroll
       for (int c = 0; c < NCL; ++c) words[c] = ~words[c] & 0xffffffu;
@@ -573,9 +563,9 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         const uint32_t my = (__float_as_uint(d1.y) >> 31) + (__float_as_uint(d2.y) >> 31) + (__float_as_uint(d3.y) >> 31);
         const uint32_t cx = (mx ^ 7u ^ sar31(__float_as_uint(u.x))) & 7u;
         const uint32_t cy = (my ^ 7u ^ sar31(__float_as_uint(u.y))) & 7u;
-        const int c0 = (p >> 3) * 2, e = p & 7;
-        words[c0] += cx << (3 * e);  // disjoint fields: + == |, one LEA
-        words[c0 + 1] += cy << (3 * e);
+        const int c = p >> 2, e = 2 * (p & 3);
+        words[c] += cx << (3 * e);  // disjoint fields: + == |, one LEA
+        words[c] += cy << (3 * e + 3);
       }
 #endif
       const float g = fminf(fminf(gacc[0], gacc[1]), fminf(gacc[2], gacc[3]));
@@ -594,7 +584,7 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
           const float t3 = p1 ? (p2 ? m[6] : m[4]) : (p2 ? m[2] : m[0]);
           const bool p3 = z > t3;
           g = fminf(g, fminf(fabsf(z - m[3]), fminf(fabsf(z - t2), fabsf(z - t3))));
-          words[(p >> 3) * 2 + hh] |= ((p1 ? 4u : 0u) | (p2 ? 2u : 0u) | (p3 ? 1u : 0u)) << (3 * (p & 7));
+          words[p >> 2] |= ((p1 ? 4u : 0u) | (p2 ? 2u : 0u) | (p3 ? 1u : 0u)) << (3 * (2 * (p & 3) + hh));
         }
       }
       replay |= g < delta;
@@ -1011,8 +1001,8 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
         const int sh = 3 * e;
         const uint32_t off = (sh <= 9 ? (words[c] << (9 - sh)) : (words[c] >> (sh - 9))) & 0xe00u;
         const float val = __uint_as_float(tma::lds32(off | lane_off));
-        if (c & 1) xp[(c >> 1) * 8 + e].y = val;
-        else xp[(c >> 1) * 8 + e].x = val;
+        if (e & 1) xp[4 * c + (e >> 1)].y = val;
+        else xp[4 * c + (e >> 1)].x = val;
       }
     }
     fwht_vector<D>(xp, s);
@@ -1039,10 +1029,10 @@ __device__ void dec_value_item(const DecArgs& a, const Item& it, uint8_t* in, in
     // swizzled staging of the output tile (TMA tensor store layout)
 #pragma unroll
     for (int c = 0; c < NCL; ++c) {
-      const int p0 = (c >> 1) * 8, gc = s * NCL + c;
+      const int gc = s * NCL + c;
       float y[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) y[e] = (c & 1) ? xp[p0 + e].y : xp[p0 + e].x;
+      for (int e = 0; e < 8; ++e) y[e] = (e & 1) ? xp[4 * c + (e >> 1)].y : xp[4 * c + (e >> 1)].x;
       if constexpr (sizeof(TOut) == 2) {
         tma::sts128(out_s + TL::off(vr, gc), make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]),
                                                         pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7])));
@@ -2140,7 +2130,8 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // 66 315; bf16: 46 246, 48 237, 50 235, 52 240 -- profiles/r02/frac3.txt)
       // (C2, d64: f32 0.42 -> 220 us, 0.459 -> 198, 0.486 -> 190, 0.514 -> 197; bf16 0.338 -> 157,
       // 0.365 -> 147.5, 0.392 -> 152 -- frac_c2*.txt)
-      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.419 : 0.34) : (eb == 4 ? 0.486 : 0.365))
+      // (after the neighbour-pair FWHT layout, C3 f32: 62 key CTAs 301.5 us, 64 294, 66 288.4, 68 294)
+      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.446 : 0.34) : (eb == 4 ? 0.5 : 0.365))
                                              : (d128 ? 0.43 : 0.46);
       if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
