@@ -519,10 +519,11 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
       // Codes from sign bits. s_k = sign(|u| - t_k N) is a thermometer code
       // (t1 < t2 < t3), mm = s1 + s2 + s3 = #thresholds above |u| has
       // bit1 = s2 and bit0 = s1^s2^s3, and code = negative ? mm : 7 - mm.
-      // So, with n = sign(u): code bits (2,1,0) = ~(n, s2^n, s1^s2^s3^n):
-      // the complemented bits are shifted into the word MSB-first (one
-      // funnel shift each, coordinate 7 of the chunk first) and the word is
-      // complemented once at the end.
+      // So, with n = sign(u): code bits (2,1,0) = ~(n, s2^n, s1^s2^s3^n).
+      // Per coordinate the raw bits (n, s2, s1^s3) are shifted into the word
+      // MSB-first (one funnel shift each, coordinate 7 of the chunk first);
+      // the XOR chain and the complement then run once per 24-bit word:
+      // bit1 ^= bit2, bit0 ^= bit1, ~ (one XOR per coordinate saved).
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
         const int p = (q & ~3) | (3 - (q & 3));  // pairs (7,6), (5,4), .. of each chunk
@@ -537,15 +538,20 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
         gb = fminf(gb, fminf(au.x, au.y));
         const int c = p >> 2;
         const uint32_t ux = __float_as_uint(u.x), uy = __float_as_uint(u.y);
-        const uint32_t b1x = __float_as_uint(d2.x) ^ ux, b1y = __float_as_uint(d2.y) ^ uy;
-        const uint32_t b0x = __float_as_uint(d1.x) ^ __float_as_uint(d3.x) ^ b1x;
-        const uint32_t b0y = __float_as_uint(d1.y) ^ __float_as_uint(d3.y) ^ b1y;
+        const uint32_t b2x = __float_as_uint(d2.x), b2y = __float_as_uint(d2.y);
+        const uint32_t b13x = __float_as_uint(d1.x) ^ __float_as_uint(d3.x);
+        const uint32_t b13y = __float_as_uint(d1.y) ^ __float_as_uint(d3.y);
         // y is the odd (higher) coordinate of the pair: its bits go in first
-        words[c] = __funnelshift_l(b0y, __funnelshift_l(b1y, __funnelshift_l(uy, words[c], 1), 1), 1);
-        words[c] = __funnelshift_l(b0x, __funnelshift_l(b1x, __funnelshift_l(ux, words[c], 1), 1), 1);
+        words[c] = __funnelshift_l(b13y, __funnelshift_l(b2y, __funnelshift_l(uy, words[c], 1), 1), 1);
+        words[c] = __funnelshift_l(b13x, __funnelshift_l(b2x, __funnelshift_l(ux, words[c], 1), 1), 1);
       }
 #pragma unroll
-      for (int c = 0; c < NCL; ++c) words[c] = ~words[c] & 0xffffffu;
+      for (int c = 0; c < NCL; ++c) {
+        uint32_t w = words[c];                // fields (n, s2, s1^s3), 24 bits
+        w ^= (w >> 1) & 0x492492u;            // bit1 = s2 ^ n
+        w ^= (w >> 1) & 0x249249u;            // bit0 = s1 ^ s3 ^ s2 ^ n
+        words[c] = w ^ 0xffffffu;             // complement (the upper 8 bits are 0)
+      }
 #else
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
