@@ -2137,7 +2137,9 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // (C2, d64: f32 0.42 -> 220 us, 0.459 -> 198, 0.486 -> 190, 0.514 -> 197; bf16 0.338 -> 157,
       // 0.365 -> 147.5, 0.392 -> 152 -- frac_c2*.txt)
       // (after the neighbour-pair FWHT layout, C3 f32: 62 key CTAs 301.5 us, 64 294, 66 288.4, 68 294)
-      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.446 : 0.34) : (eb == 4 ? 0.5 : 0.365))
+      // (after the word-level code XORs: C3 f32 66 -> 287.6 us, 68 -> 281.9, 70 -> 284; bf16 50 -> 229.8,
+      // 52 -> 222.7, 54 -> 228; C2 f32 0.5 -> 187.5, 0.527 -> 181.7; bf16 0.365 -> 149, 0.392 -> 141.2)
+      double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.459 : 0.351) : (eb == 4 ? 0.527 : 0.392))
                                              : (d128 ? 0.43 : 0.46);
       if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
