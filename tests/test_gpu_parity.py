@@ -381,13 +381,16 @@ def test_role_splits_and_schedules_do_not_change_results(monkeypatch, mode):
     ref_out = ref.attach(16).materialize_all()
     # (also the co-resident encode kernel, PKV_ENC_ROLES=co, against the
     # default role-split one; SM shares only matter to the split kernel)
+    # ("absval": the per-tensor absmax items run on the value CTAs, PKV_ABSMAX_ROLE=values)
     for enc_frac, dec_frac, lag, roles in [("0.1", "0.1", "1", "split"), ("0.6", "0", "2", "split"),
                                            ("0.9", "0.9", "8", "split"), ("0.3", "0.3", "1", "co"),
-                                           ("0.3", "0.3", "7", "co")]:
+                                           ("0.3", "0.3", "7", "co"), ("0.3", "0.3", "2", "absval"),
+                                           ("0.05", "0.3", "3", "absval")]:
         monkeypatch.setenv("PKV_KEY_SM_FRACTION", enc_frac)
         monkeypatch.setenv("PKV_DEC_KEY_FRACTION", dec_frac)
         monkeypatch.setenv("PKV_KEY_LAG", lag)
-        monkeypatch.setenv("PKV_ENC_ROLES", roles)
+        monkeypatch.setenv("PKV_ENC_ROLES", "split" if roles == "absval" else roles)
+        monkeypatch.setenv("PKV_ABSMAX_ROLE", "values" if roles == "absval" else "keys")
         _lib.reload_tuning()  # knobs are read once per process otherwise
         p = pk.build_pool(dump, k_scale_mode=mode)
         for i in range(g.num_layers):
