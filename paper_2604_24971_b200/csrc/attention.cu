@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
     else cp_async_wait_all();
     __syncthreads();  // raw tile landed; every warp is done with the previous K / Y tiles
     // ---- K: int8 codes -> f16 (exact; block32: x f16 scale), 16 codes per thread-step ----
+#ifndef PKV_ATTN_SKIP_K  // (timing experiment)
     for (int i = tid; i < TT * D / 16; i += 128) {
       const int t = i / (D / 16), c = i % (D / 16);
       uint4 w = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // code 0
@@ -531,7 +532,9 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
       *reinterpret_cast<uint4*>(kh + sw<D>(t, 2 * c)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
       *reinterpret_cast<uint4*>(kh + sw<D>(t, 2 * c + 1)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
     }
+#endif
     // ---- V: 3-bit codes -> centroid hi / lo f16 tiles; rms per token ----
+#ifndef PKV_ATTN_SKIP_V  // (timing experiment: PKV_ATTN_SKIP_V=1 leaves the V tiles unconverted)
     for (int i = tid; i < TT * D / 8; i += 128) {
       const int t = i / (D / 8), c = i % (D / 8);
       uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
@@ -549,6 +552,7 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
       *reinterpret_cast<uint4*>(yhi + sw<D>(t, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(ylo + sw<D>(t, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
+#endif
     for (int i = tid; i < TT; i += 128) rms_s[i] = i < nt ? rs[i] : 0.f;
     __syncthreads();  // tiles converted; this raw buffer is free for tile i + 2
     if (t0 + 2 * TT < t_end) stage(t0 + 2 * TT, (int)min((long long)TT, t_end - t0 - 2 * TT), raw);
