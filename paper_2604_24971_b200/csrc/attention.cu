@@ -535,22 +535,34 @@ __global__ void __launch_bounds__(128) prefix_mma(const __grid_constant__ Args a
 #endif
     // ---- V: 3-bit codes -> centroid hi / lo f16 tiles; rms per token ----
 #ifndef PKV_ATTN_SKIP_V  // (timing experiment: PKV_ATTN_SKIP_V=1 leaves the V tiles unconverted)
-    for (int i = tid; i < TT * D / 8; i += 128) {
-      const int t = i / (D / 8), c = i % (D / 8);
-      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+    // (four packed 24-bit words = 32 codes per step, read as three aligned
+    // 32-bit words instead of twelve bytes)
+    for (int i = tid; i < TT * D / 32; i += 128) {
+      const int t = i / (D / 32), cg = i % (D / 32);
+      uint32_t wd[4] = {0, 0, 0, 0};
       if (t < nt) {
-        const uint8_t* p = rv + t * (3 * D / 8) + 3 * c;
-        const uint32_t word = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const uint32_t x0 = ctab[((word >> (3 * e)) & 7u) * 128 + tid];
-          const uint32_t x1 = ctab[((word >> (3 * e + 3)) & 7u) * 128 + tid];
-          hi[e / 2] = __byte_perm(x0, x1, 0x5410);
-          lo[e / 2] = __byte_perm(x0, x1, 0x7632);
-        }
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(rv + t * (3 * D / 8) + 12 * cg);
+        const uint32_t u0 = p[0], u1 = p[1], u2 = p[2];
+        wd[0] = u0 & 0xffffffu;
+        wd[1] = __funnelshift_r(u0, u1, 24) & 0xffffffu;
+        wd[2] = __funnelshift_r(u1, u2, 16) & 0xffffffu;
+        wd[3] = u2 >> 8;
       }
-      *reinterpret_cast<uint4*>(yhi + sw<D>(t, c)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(ylo + sw<D>(t, c)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+        if (t < nt) {
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const uint32_t x0 = ctab[((wd[q] >> (3 * e)) & 7u) * 128 + tid];
+            const uint32_t x1 = ctab[((wd[q] >> (3 * e + 3)) & 7u) * 128 + tid];
+            hi[e / 2] = __byte_perm(x0, x1, 0x5410);
+            lo[e / 2] = __byte_perm(x0, x1, 0x7632);
+          }
+        }
+        *reinterpret_cast<uint4*>(yhi + sw<D>(t, 4 * cg + q)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(ylo + sw<D>(t, 4 * cg + q)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
     }
 #endif
     for (int i = tid; i < TT; i += 128) rms_s[i] = i < nt ? rs[i] : 0.f;
