@@ -408,3 +408,50 @@ def test_nonfinite_key_in_a_full_item_raises(dtype, bad):
     k = dump.layers[1][0]
     with pytest.raises(pk.GeometryError, match="NaN or Inf"):
         pk.quantize_k(k)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_more_layers_than_one_launch_holds(dtype):
+    # Llama-70B has 80 layers: pkv_encode / pkv_decode split into launches of
+    # PKV_MAX_LAYERS_PER_LAUNCH (64) layers; the per-tensor key maxima, the
+    # layer-major arena and the decode must line up across the boundary
+    g = pk.ModelGeometry(num_layers=80, kv_heads=2, head_dim=128, seq_len=24)
+    dump = pk.synth_gaussian_dump(g, seed=80, device="cuda", dtype=dtype)
+    pool = pk.build_pool(dump, sign_seed=2)
+    assert len(pool.build_stats) == 80
+    view = pool.attach(32)
+    outs = view.materialize_all()
+    for li in (0, 62, 63, 64, 65, 79):
+        k_in, v_in = (t.values.float().cpu().numpy() for t in dump.layers[li])
+        s, kc = O.quantize_k_tensor(k_in)
+        vc, vs = O.quantize_v(v_in, sign_seed=2)
+        kq, vq = pool.layer_blocks(li)
+        assert np.float32(kq.scale) == np.float32(s) and np.array_equal(host(kq.codes), kc), li
+        assert np.array_equal(host(vq.codes), vc) and np.array_equal(host(vq.scales).view(np.uint32), vs.view(np.uint32)), li
+        kw, vw = O.decode_layer(kc, s, vc, vs, decode_bits=32, sign_seed=2)
+        assert np.array_equal(host(outs[li][0]).view(np.uint32), kw.view(np.uint32)), li
+        assert np.array_equal(host(outs[li][1]).view(np.uint32), vw.view(np.uint32)), li
+        k1, v1 = view.get_kv_for_layer(li)
+        assert torch.equal(k1.values, outs[li][0]) and torch.equal(v1.values, outs[li][1])
+
+
+def test_non_contiguous_and_host_inputs_encode_like_contiguous_ones():
+    # a KV cache laid out [B, T, H, D] (transformers' key_states before the
+    # transpose) viewed as [B, H, T, D], and plain host numpy arrays: the
+    # reference takes any array; the device path must give the same pool
+    g = pk.ModelGeometry(num_layers=2, kv_heads=4, head_dim=64, seq_len=33)
+    rng = np.random.default_rng(5)
+    layers_np = [(rng.normal(size=g.tensor_shape).astype(np.float32),
+                  rng.normal(size=g.tensor_shape).astype(np.float32)) for _ in range(2)]
+    as_bthd = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(0, 2, 1, 3))).cuda().transpose(1, 2)
+    assert not as_bthd(layers_np[0][0]).is_contiguous()
+    strided = pk.KvDump(g, tuple((pk.KvTensor(g, as_bthd(k)), pk.KvTensor(g, as_bthd(v))) for k, v in layers_np))
+    host_dump = pk.KvDump(g, tuple((pk.KvTensor(g, k), pk.KvTensor(g, v)) for k, v in layers_np))
+    a, b = pk.build_pool(strided), pk.build_pool(host_dump)
+    for i, (k, v) in enumerate(layers_np):
+        s, kc = O.quantize_k_tensor(k)
+        vc, vs = O.quantize_v(v)
+        for p in (a, b):
+            kq, vq = p.layer_blocks(i)
+            assert np.float32(kq.scale) == np.float32(s) and np.array_equal(host(kq.codes), kc)
+            assert np.array_equal(host(vq.codes), vc) and np.array_equal(host(vq.scales).view(np.uint32), vs.view(np.uint32))
