@@ -455,3 +455,23 @@ def test_non_contiguous_and_host_inputs_encode_like_contiguous_ones():
             kq, vq = p.layer_blocks(i)
             assert np.float32(kq.scale) == np.float32(s) and np.array_equal(host(kq.codes), kc)
             assert np.array_equal(host(vq.codes), vc) and np.array_equal(host(vq.scales).view(np.uint32), vs.view(np.uint32))
+
+
+@pytest.mark.parametrize("scale", [1e-38, 1e-25, 1e-12, 1e12, 1e25, 1e30])
+def test_extreme_magnitudes_code_like_the_oracle(scale):
+    # per-vector norms far from 1 (sub-normal-ish and huge): the fast path
+    # hands vectors with sum(x^2) outside [2^-200, 2^200] to the exact replay,
+    # keys below a 1e-30 scale to the exact key path; everything must match
+    # the f64 reference, decode included
+    x = (np.random.default_rng(int(abs(np.log10(scale)))).normal(size=(1, 3, 21, 128)) * scale).astype(np.float32)
+    k = (np.random.default_rng(7).normal(size=(1, 3, 21, 128)) * scale).astype(np.float32)
+    t, tk = value_tensor(x), value_tensor(k)
+    block = pk.quantize_v(t)
+    assert_v_matches_oracle(t, block)
+    codes, scales = O.quantize_v(x)
+    want = O.dequantize_v(codes, scales)
+    assert np.array_equal(host(pk.dequantize_v(block).values).view(np.uint32), want.view(np.uint32))
+    kb = pk.quantize_k(tk)
+    assert_k_matches_oracle(tk, kb)
+    s, kc = O.quantize_k_tensor(k)
+    assert np.array_equal(host(pk.dequantize_k(kb).values).view(np.uint32), O.dequantize_k_tensor(kc, s).view(np.uint32))
