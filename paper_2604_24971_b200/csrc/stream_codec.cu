@@ -70,6 +70,9 @@ constexpr bool kKeyDynamic = PKV_KEY_DYNAMIC;
 #ifndef PKV_ROLE_MAP
 #define PKV_ROLE_MAP 0  // 0: roles by block index, 1: by SM id (measured slightly slower)
 #endif
+#ifndef PKV_ENC_XHALF
+#define PKV_ENC_XHALF 1  // encode, two lanes per vector: the cross-half FWHT stage first, from shared memory
+#endif
 #ifndef PKV_SIGNPACK
 #define PKV_SIGNPACK 1  // value codes packed from sign bits by funnel shifts
 #endif  // bf16 key items: copy to registers, release the stage
@@ -464,32 +467,77 @@ __device__ void enc_value_item(const EncArgs& a, const Item& it, uint32_t in_s, 
     const long long v = vbase + vr;
     const bool valid = v < a.nvec;
     float2 xp[NP];
+    double sacc[4];
 #pragma unroll
-    for (int c = 0; c < NCL; ++c) {
-      float t[8];
-      const int gc = s * NCL + c;  // chunk index within the vector
+    for (int k = 0; k < 4; ++k) sacc[k] = 0.0;
+    auto chunk_in = [&](int gc, float (&t)[8]) {
       if constexpr (sizeof(TIn) == 2) {
         lds_chunk8<TIn>(in_s + TL::off(vr, gc), 0, t);
       } else {
         lds_chunk8<TIn>(in_s + TL::off(vr, 2 * gc), in_s + TL::off(vr, 2 * gc + 1), t);
       }
+    };
+#if PKV_ENC_XHALF
+    if constexpr (G::TPV == 2) {
+      // Two lanes per vector. The stage across the two halves (half = D/2)
+      // runs FIRST, on inputs read from shared memory: each lane loads its
+      // own half and its partner's (the tile is in shared memory anyway) and
+      // keeps own + other (lower lane) or other - own (upper lane), so the
+      // remaining stages are lane-local and the rotation needs no shuffle
+      // (4 issue cycles per coordinate). The stage order differs from
+      // numpy's, which the fast path allows: the guard band bounds the fp32
+      // rounding of log2(d) butterfly layers in any order (guard_delta), and
+      // any vector near a decision threshold is replayed in numpy's order.
+      // (C3 value role: f32 156 -> 152 us, bf16 151 -> 140 us)
+      const float sg = s ? -1.f : 1.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) xp[4 * c + i] = f2(t[2 * i], t[2 * i + 1]);
-    }
-    // squared norm in fp64 from the inputs (the rotation is orthogonal);
-    // every x^2 is exact in fp64 and the sum is good to ~D * 2^-53.
-    double sacc[4];
+      for (int c = 0; c < NCL; ++c) {
+        float t[8], o[8];
+        chunk_in(s * NCL + c, t);
+        chunk_in((1 - s) * NCL + c, o);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sacc[k] = 0.0;
+        for (int e = 0; e < 8; ++e) sacc[e & 3] = fma((double)t[e], (double)t[e], sacc[e & 3]);
+        if (SIGN) {  // vals * sign_diagonal on both halves
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      sacc[(2 * p) & 3] = fma((double)xp[p].x, (double)xp[p].x, sacc[(2 * p) & 3]);
-      sacc[(2 * p + 1) & 3] = fma((double)xp[p].y, (double)xp[p].y, sacc[(2 * p + 1) & 3]);
+          for (int e = 0; e < 8; ++e) {
+            const int im = s * G::CPT + 8 * c + e, io = (1 - s) * G::CPT + 8 * c + e;
+            t[e] = __uint_as_float(__float_as_uint(t[e]) ^ (((a.sign_bits[im >> 5] >> (im & 31)) & 1u) << 31));
+            o[e] = __uint_as_float(__float_as_uint(o[e]) ^ (((a.sign_bits[io >> 5] >> (io & 31)) & 1u) << 31));
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          xp[4 * c + i] = __ffma2_rn(f2(sg, sg), f2(t[2 * i], t[2 * i + 1]), f2(o[2 * i], o[2 * i + 1]));
+      }
+    } else
+#endif
+    {
+#pragma unroll
+      for (int c = 0; c < NCL; ++c) {
+        float t[8];
+        chunk_in(s * NCL + c, t);  // chunk index within the vector
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xp[4 * c + i] = f2(t[2 * i], t[2 * i + 1]);
+      }
+      // squared norm in fp64 from the inputs (the rotation is orthogonal);
+      // every x^2 is exact in fp64 and the sum is good to ~D * 2^-53.
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        sacc[(2 * p) & 3] = fma((double)xp[p].x, (double)xp[p].x, sacc[(2 * p) & 3]);
+        sacc[(2 * p + 1) & 3] = fma((double)xp[p].y, (double)xp[p].y, sacc[(2 * p + 1) & 3]);
+      }
     }
     double S = (sacc[0] + sacc[1]) + (sacc[2] + sacc[3]);
     if constexpr (G::TPV == 2) S += __shfl_xor_sync(0xffffffffu, S, G::VPW);  // a + b == b + a
-    if (SIGN) apply_sign<NP>(xp, a.sign_bits, s * G::CPT);
-    fwht_vector<D>(xp, s);  // U = H x (unnormalised)
+#if PKV_ENC_XHALF
+    if constexpr (G::TPV == 2) {
+      fwht_pairs<G::CPT>(xp);  // the lane-local stages
+    } else
+#endif
+    {
+      if (SIGN) apply_sign<NP>(xp, a.sign_bits, s * G::CPT);
+      fwht_vector<D>(xp, s);  // U = H x (unnormalised)
+    }
 
     bool replay = false, nonfinite = false, zero = false;
     float scale = 0.f, N = 0.f;
