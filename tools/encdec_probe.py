@@ -42,3 +42,17 @@ print("enc,enc", run([(E, "e"), (E, "e")]))
 print("enc,dec", run([(E, "e"), (Dd, "d")]))
 print("enc,junkwrite,dec", run([(E, "e"), (lambda: junk.fill_(1), "j"), (Dd, "d")]))
 print("dec,junkread?,enc", run([(Dd, "d"), (lambda: junk.sum(), "r"), (E, "e")]))
+ED = graph(lambda: (enc(), dec()))
+print("one graph enc+dec", run([(ED, "ed")]))
+print("two graphs enc,dec", run([(E, "e"), (Dd, "d")]))
+def run_noev(seq, n=30):
+    for _ in range(3):
+        for f in seq: f()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        for f in seq: f()
+    b.record(); torch.cuda.synchronize()
+    return round(a.elapsed_time(b) / n * 1e3, 1)
+print("no events: two graphs", run_noev([E, Dd]), "one graph", run_noev([ED]))
