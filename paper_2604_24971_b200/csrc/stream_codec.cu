@@ -2188,7 +2188,7 @@ int encode(const EncodeRequest& r, cudaStream_t st) {
       // (after the word-level code XORs: C3 f32 66 -> 287.6 us, 68 -> 281.9, 70 -> 284; bf16 50 -> 229.8,
       // 52 -> 222.7, 54 -> 228; C2 f32 0.5 -> 187.5, 0.527 -> 181.7; bf16 0.365 -> 149, 0.392 -> 141.2)
       double frac = r.k_mode == PKV_K_TENSOR ? (d128 ? (eb == 4 ? 0.459 : 0.351) : (eb == 4 ? 0.527 : 0.392))
-                                             : (d128 ? 0.43 : 0.46);
+                                             : (d128 ? (eb == 4 ? 0.446 : 0.43) : 0.46);  // block32 C3 f32: 62 -> 268.5, 66 -> 264.6, 68 -> 269.2 us
       if (a->abs_lead > 0) frac = d128 ? 0.27 : 0.3;  // the key role only encodes
       if (tuning().key_sm_fraction >= 0.0) frac = tuning().key_sm_fraction;
       // an even count: the two SMs of a TPC must run the same role (an odd
