@@ -975,6 +975,14 @@ __device__ void dec_key_item(const DecArgs& a, const Item& it, uint32_t in_s, ui
 }
 
 // NW packed 24-bit words (chunk order) from shared or global memory
+// The block32 key decode as a separate (non-inlined) function: inlined, its
+// register demand spilled in the value path of the same kernel (value decode
+// 88 -> 107 us in block32 launches).
+template <typename TOut>
+__device__ __noinline__ void dec_key_item_b32(const DecArgs& a, const Item& it, uint32_t in_s, uint8_t* out, int gt) {
+  dec_key_item<TOut, true>(a, it, in_s, out, gt);
+}
+
 template <int NW>
 __device__ __forceinline__ void load_packed(const uint8_t* p, bool smem, uint32_t (&w)[NW]) {
   if constexpr (NW % 4 == 0) {
@@ -1872,7 +1880,8 @@ __global__ void __launch_bounds__(threads_for<dec_groups<TOut>()>(), 1) dec_kern
     int nv = 0;
     long long v0 = 0;
     if (it.kind == kKeyDec) {
-      dec_key_item<TOut, B32>(a, it, tma::smem_u32(in), out, gt);
+      if constexpr (B32) dec_key_item_b32<TOut>(a, it, tma::smem_u32(in), out, gt);
+      else dec_key_item<TOut, false>(a, it, tma::smem_u32(in), out, gt);
     } else {
       v0 = (long long)it.idx * TL::VR;
       nv = (int)min((long long)TL::VR, a.nvec - v0);
@@ -2265,6 +2274,8 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
     // C2 (d64, cheaper value path) 0 -> 109 us, 0.35 -> 96, 0.4 -> 89, 0.45 -> 97.
     // PKV_DEC_KEY_FRACTION overrides (0 = interleaved items on every SM)
     double frac = r.head_dim >= 128 ? 0.35 : 0.39;  // (C2 with even counts: 0.378 -> 90.3, 0.392 -> 88.6, 0.405 -> 91.0)
+    // block32 keys (per-32 fp16 scales): C3 0.35 -> 172.6 us, 0.4 -> 150.7, 0.45 -> 154.2
+    if (r.k_mode == PKV_K_BLOCK32 && r.head_dim >= 128) frac = 0.4;
     if (tuning().dec_key_fraction >= 0.0) frac = tuning().dec_key_fraction;
     const int grid = sm_count();
     if (frac > 0.0) a->key_ctas = std::max(2, std::min(grid - 2, 2 * (int)std::lround(frac * grid / 2.0)));  // even: whole TPCs
