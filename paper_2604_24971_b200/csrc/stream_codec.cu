@@ -2273,7 +2273,8 @@ int decode(const DecodeRequest& r, cudaStream_t st) {
     // 0 (interleaved items) -> 180 us, 0.3 -> 164, 0.35 -> 140, 0.39 -> 147;
     // C2 (d64, cheaper value path) 0 -> 109 us, 0.35 -> 96, 0.4 -> 89, 0.45 -> 97.
     // PKV_DEC_KEY_FRACTION overrides (0 = interleaved items on every SM)
-    double frac = r.head_dim >= 128 ? 0.35 : 0.39;  // (C2 with even counts: 0.378 -> 90.3, 0.392 -> 88.6, 0.405 -> 91.0)
+    double frac = r.head_dim >= 128 ? 0.365 : 0.39;  // (C2 with even counts: 0.378 -> 90.3, 0.392 -> 88.6, 0.405 -> 91.0)
+    // (C3 after the round-2 value-path changes: 50 key CTAs 145.5 us, 52 ~140, 54 135.4, 56 136.7)
     // block32 keys (per-32 fp16 scales): C3 0.35 -> 172.6 us, 0.4 -> 150.7, 0.45 -> 154.2
     if (r.k_mode == PKV_K_BLOCK32 && r.head_dim >= 128) frac = 0.4;
     if (tuning().dec_key_fraction >= 0.0) frac = tuning().dec_key_fraction;
