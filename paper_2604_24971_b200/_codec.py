@@ -104,13 +104,14 @@ def encode(
     ws_bytes = lib.pkv_encode_workspace_bytes(L, num_vectors, head_dim)
     ws = torch.empty((ws_bytes + 3) // 4, dtype=torch.int32, device=device)
     arr = lambda ts: None if ts is None else ptr_array([_p(t) for t in ts])  # noqa: E731
-    rc = lib.pkv_encode(
-        L, num_vectors, head_dim, dt,
-        arr(k_in), arr(v_in), k_mode,
-        arr(k_codes), arr(k_scale), arr(k_bscale), arr(v_packed), arr(v_scales),
-        centroid_array(centroids), sign_word_array(sign_seed, head_dim),
-        status.data_ptr(), _p(replay), _p(k_layer_max), ws.data_ptr(), ws_bytes, stream_ptr(device),
-    )
+    with torch.cuda.device(device):  # the library launches on the current device
+        rc = lib.pkv_encode(
+            L, num_vectors, head_dim, dt,
+            arr(k_in), arr(v_in), k_mode,
+            arr(k_codes), arr(k_scale), arr(k_bscale), arr(v_packed), arr(v_scales),
+            centroid_array(centroids), sign_word_array(sign_seed, head_dim),
+            status.data_ptr(), _p(replay), _p(k_layer_max), ws.data_ptr(), ws_bytes, stream_ptr(device),
+        )
     check(rc, "pkv_encode")
 
 
@@ -120,8 +121,9 @@ def k_absmax(k_in: list[torch.Tensor], out: torch.Tensor, device: torch.device) 
     for t in k_in:
         if t.device != device or not t.is_contiguous() or t.dtype != k_in[0].dtype:
             raise ValueError("absmax inputs must be contiguous same-dtype tensors on the device")
-    rc = lib.pkv_k_absmax(len(k_in), k_in[0].numel(), dtype_code(k_in[0]), ptr_array([t.data_ptr() for t in k_in]),
-                          out.data_ptr(), stream_ptr(device))
+    with torch.cuda.device(device):
+        rc = lib.pkv_k_absmax(len(k_in), k_in[0].numel(), dtype_code(k_in[0]),
+                              ptr_array([t.data_ptr() for t in k_in]), out.data_ptr(), stream_ptr(device))
     check(rc, "pkv_k_absmax")
     return out
 
@@ -146,23 +148,26 @@ def decode(
     lib = load()
     L = len(k_codes if k_codes is not None else v_packed)
     arr = lambda ts: None if ts is None else ptr_array([_p(t) for t in ts])  # noqa: E731
-    rc = lib.pkv_decode(
-        L, num_vectors, head_dim, _DTYPE_CODE[out_dtype], k_mode,
-        arr(k_codes), arr(k_scale), arr(k_bscale), arr(v_packed), arr(v_scales),
-        centroid_array(centroids), sign_word_array(sign_seed, head_dim),
-        arr(k_out), arr(v_out), stream_ptr(device),
-    )
+    with torch.cuda.device(device):
+        rc = lib.pkv_decode(
+            L, num_vectors, head_dim, _DTYPE_CODE[out_dtype], k_mode,
+            arr(k_codes), arr(k_scale), arr(k_bscale), arr(v_packed), arr(v_scales),
+            centroid_array(centroids), sign_word_array(sign_seed, head_dim),
+            arr(k_out), arr(v_out), stream_ptr(device),
+        )
     check(rc, "pkv_decode")
 
 
 def unpack_codes(packed: torch.Tensor, count: int, out: torch.Tensor) -> None:
-    rc = load().pkv_unpack_codes(packed.data_ptr(), count, out.data_ptr(), stream_ptr(packed.device))
+    with torch.cuda.device(packed.device):
+        rc = load().pkv_unpack_codes(packed.data_ptr(), count, out.data_ptr(), stream_ptr(packed.device))
     check(rc, "pkv_unpack_codes")
 
 
 def pack_codes(codes: torch.Tensor, count: int, out: torch.Tensor, bad: torch.Tensor) -> None:
-    rc = load().pkv_pack_codes(codes.data_ptr(), count, out.data_ptr(), bad.data_ptr(),
-                               stream_ptr(codes.device))
+    with torch.cuda.device(codes.device):
+        rc = load().pkv_pack_codes(codes.data_ptr(), count, out.data_ptr(), bad.data_ptr(),
+                                   stream_ptr(codes.device))
     check(rc, "pkv_pack_codes")
 
 

@@ -71,17 +71,18 @@ def decode_attention(pool: SharedPool, layer: int, q: torch.Tensor, *, tail_k: t
     else:
         cap = 0
     scale = float(softmax_scale if softmax_scale is not None else D ** -0.5)
-    rc = lib.pkv_decode_attention(
-        R, H, G, D, g.seq_len, _DT[q.dtype], q.data_ptr(), K_MODES[kq.mode], kq.codes.data_ptr(),
-        kq.scale_t.data_ptr() if kq.mode == "tensor" else None,
-        kq.block_scales.data_ptr() if kq.mode == "block32" else None,
-        vq.packed.data_ptr(), vq.scales.data_ptr(), _codec.centroid_array(pool.codebook.centroids),
-        _codec.sign_word_array(pool.sign_seed, D),
-        tail_k.data_ptr() if tail_len is not None else None,
-        tail_v.data_ptr() if tail_len is not None else None,
-        tail_len.data_ptr() if tail_len is not None else None, cap, q_len, scale, _DT[out.dtype],
-        out.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
-        _codec.stream_ptr(dev))
+    with torch.cuda.device(dev):  # the library launches on the current device
+        rc = lib.pkv_decode_attention(
+            R, H, G, D, g.seq_len, _DT[q.dtype], q.data_ptr(), K_MODES[kq.mode], kq.codes.data_ptr(),
+            kq.scale_t.data_ptr() if kq.mode == "tensor" else None,
+            kq.block_scales.data_ptr() if kq.mode == "block32" else None,
+            vq.packed.data_ptr(), vq.scales.data_ptr(), _codec.centroid_array(pool.codebook.centroids),
+            _codec.sign_word_array(pool.sign_seed, D),
+            tail_k.data_ptr() if tail_len is not None else None,
+            tail_v.data_ptr() if tail_len is not None else None,
+            tail_len.data_ptr() if tail_len is not None else None, cap, q_len, scale, _DT[out.dtype],
+            out.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+            _codec.stream_ptr(dev))
     check(rc, "pkv_decode_attention")
     return out
 

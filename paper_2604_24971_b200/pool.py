@@ -653,11 +653,12 @@ def compute_layer_stats(dump: KvDump, pool: SharedPool, chunk: int = 8) -> tuple
         if len(dt) != 1 or dt.pop() not in (torch.float32, torch.bfloat16):
             ks = [t.float() for t in ks]
             vs = [t.float() for t in vs]
-        rc = lib.pkv_layer_stats(
-            len(idx), n, _codec.dtype_code(ks[0]), ptr_array([t.data_ptr() for t in ks]),
-            ptr_array([t.data_ptr() for t in vs]), ptr_array([k.data_ptr() for k, _ in decoded]),
-            ptr_array([v.data_ptr() for _, v in decoded]), sums[c0].data_ptr(), ws.data_ptr(),
-            ws.numel() * 8, _codec.stream_ptr(dev))
+        with torch.cuda.device(dev):
+            rc = lib.pkv_layer_stats(
+                len(idx), n, _codec.dtype_code(ks[0]), ptr_array([t.data_ptr() for t in ks]),
+                ptr_array([t.data_ptr() for t in vs]), ptr_array([k.data_ptr() for k, _ in decoded]),
+                ptr_array([v.data_ptr() for _, v in decoded]), sums[c0].data_ptr(), ws.data_ptr(),
+                ws.numel() * 8, _codec.stream_ptr(dev))
         check(rc, "pkv_layer_stats")
     host = sums.cpu().numpy()
     stats = []
