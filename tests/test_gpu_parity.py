@@ -6,6 +6,8 @@ attention within 1e-3 relative of an fp64 oracle.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -330,13 +332,13 @@ def test_config2_shape_sampled_layers_bit_exact():
         assert np.array_equal(u32(dec[li][1]), vd.view(np.uint32))
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PKV_STRESS_SEEDS", "16"))))
 def test_random_shapes_tails_and_modes_bit_exact(seed):
     """Ragged shapes through the TMA paths: token counts that leave partial
     tiles / partial bulk copies, every supported head_dim, bf16 and f32 inputs,
     both key modes, sign diagonals; everything bit-exact vs the oracle."""
     rng = np.random.default_rng(100 + seed)
-    D = int(rng.choice([16, 32, 64, 128]))
+    D = int(rng.choice([1, 2, 4, 8, 16, 32, 64, 64, 128, 128, 128, 256]))
     H = int(rng.integers(1, 5))
     T = int(rng.integers(1, 700))
     L = int(rng.integers(1, 4))
