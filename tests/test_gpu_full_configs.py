@@ -15,6 +15,7 @@ and the sign diagonal. Also the FMA-adversarial replay vectors
 
 from __future__ import annotations
 
+import os
 from pathlib import Path
 
 import numpy as np
@@ -236,3 +237,46 @@ def test_multi_token_step_is_causal_over_the_tail(q_len):
         got = out.reshape(R, H, G, q_len, D)[:, :, :, i]
         worst = max(worst, np.abs(got - want).max() / np.abs(want).max())
     assert worst < 1e-3, worst
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PKV_ATTN_STRESS_SEEDS", "6"))))
+def test_random_attention_shapes_vs_oracle(seed):
+    """Random decode-attention problems through the tensor-core kernel: KV
+    heads, head_dim 64/128, ragged T (partial tiles, T below one tile), agent
+    and group counts (row tiles of 16/32/64, partial), bf16/f32 queries, tails
+    with random lengths, block32 keys and the sign diagonal; within 1e-3 of an
+    fp64 softmax over the oracle's decode. PKV_ATTN_STRESS_SEEDS widens it."""
+    from paper_2604_24971_b200 import attention as A
+
+    rng = np.random.default_rng(900 + seed)
+    D = int(rng.choice([64, 128]))
+    H = int(rng.choice([1, 2, 4, 8]))
+    T = int(rng.integers(1, 3000))
+    R = int(rng.integers(1, 17))
+    G = int(rng.choice([1, 2, 4, 8]))
+    k_mode = "block32" if seed % 3 == 2 else "tensor"
+    sign_seed = 3 if seed % 4 == 1 else None
+    qdt = torch.bfloat16 if seed % 2 else torch.float32
+    g = pk.ModelGeometry(num_layers=1, kv_heads=H, head_dim=D, seq_len=T)
+    host = O.synth_dump(1, H, D, T, seed=seed)
+    dump = device_dump(g, host, torch.float32)
+    pool = pk.build_pool(dump, build_stats=False, k_scale_mode=k_mode, sign_seed=sign_seed)
+    w = check_pool_layers(pool, dump, [0], k_mode=k_mode, sign_seed=sign_seed)[0]
+    kd, vd = O.decode_layer(w["k_codes"], w.get("k_scale", 0.0), w["v_codes"], w["v_scales"], 32,
+                            sign_seed=sign_seed, k_block_scales=w.get("k_bscale"))
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.randn(R, H, G, D, device="cuda", generator=gen).to(qdt)
+    cap = int(rng.integers(0, 24))
+    kw = {}
+    tails_k = tails_v = None
+    if cap:
+        tail_len = torch.randint(0, cap + 1, (R,), device="cuda", dtype=torch.int32, generator=gen)
+        tk = torch.randn(R, H, cap, D, device="cuda", generator=gen).bfloat16()
+        tv = torch.randn(R, H, cap, D, device="cuda", generator=gen).bfloat16()
+        kw = dict(tail_k=tk, tail_v=tv, tail_len=tail_len)
+        tails_k = [tk[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
+        tails_v = [tv[r, :, : int(tail_len[r])].float().cpu().numpy() for r in range(R)]
+    out = A.decode_attention(pool, 0, q, softmax_scale=D ** -0.5, out_dtype=torch.float32, **kw)
+    want = O.attention_over_pool(q.float().cpu().numpy(), kd[0], vd[0], D ** -0.5, tails_k, tails_v)
+    rel = np.abs(out.cpu().numpy().astype(np.float64) - want).max() / np.abs(want).max()
+    assert rel < 1e-3, (rel, D, H, T, R, G, k_mode, sign_seed, cap)
