@@ -475,3 +475,83 @@ def test_extreme_magnitudes_code_like_the_oracle(scale):
     assert_k_matches_oracle(tk, kb)
     s, kc = O.quantize_k_tensor(k)
     assert np.array_equal(host(pk.dequantize_k(kb).values).view(np.uint32), O.dequantize_k_tensor(kc, s).view(np.uint32))
+
+
+def _canary_views(nbytes_list, dtype_list, device, pad=256, fill=0xA5):
+    """One buffer per request, each carved at a 256-byte aligned offset out of
+    a larger canary-filled byte buffer; returns (views, checker)."""
+    bufs, views = [], []
+    for nbytes, dt in zip(nbytes_list, dtype_list):
+        big = torch.full((pad + ((nbytes + 255) // 256) * 256 + pad,), fill, dtype=torch.uint8, device=device)
+        view = big[pad:pad + nbytes].view(dt)
+        bufs.append((big, nbytes))
+        views.append(view)
+
+    def intact():
+        for big, nbytes in bufs:
+            b = big.cpu().numpy()
+            if (b[:pad] != fill).any() or (b[pad + nbytes:] != fill).any():
+                return False
+        return True
+    return views, intact
+
+
+@pytest.mark.parametrize("D,H,T,dtype", [(128, 3, 37, torch.float32), (64, 5, 23, torch.bfloat16),
+                                          (2, 1, 7, torch.float32), (16, 2, 9, torch.bfloat16)])
+def test_kernels_write_exactly_the_documented_bytes(D, H, T, dtype):
+    # compute-sanitizer is not available on this GPU pool: instead every output
+    # of pkv_encode / pkv_decode is a view at an aligned offset inside a larger
+    # canary-filled buffer, sized exactly as include/polykv.h documents (n key
+    # codes, 3*ceil(n/8) packed bytes, one f32 scale per head vector, n
+    # outputs); nothing around them may change
+    from paper_2604_24971_b200 import _codec
+    from paper_2604_24971_b200.keyquant import K_MODES
+
+    L, dev = 2, torch.device("cuda", torch.cuda.current_device())
+    nvec, n = H * T, H * T * D
+    rng = np.random.default_rng(D + T)
+    ks = [torch.from_numpy(rng.normal(size=n).astype(np.float32)).to(dev, dtype) for _ in range(L)]
+    vs = [torch.from_numpy(rng.normal(size=n).astype(np.float32)).to(dev, dtype) for _ in range(L)]
+    pk_bytes = 3 * ((n + 7) // 8)
+    views, intact = _canary_views([n] * L + [4] * L + [pk_bytes] * L + [4 * nvec] * L,
+                                  [torch.int8] * L + [torch.float32] * L + [torch.uint8] * L + [torch.float32] * L, dev)
+    k_codes, k_scale, v_packed, v_scales = views[:L], views[L:2 * L], views[2 * L:3 * L], views[3 * L:]
+    status = torch.zeros(L, dtype=torch.int32, device=dev)
+    _codec.encode(num_vectors=nvec, head_dim=D, k_in=ks, v_in=vs, k_mode=K_MODES["tensor"], k_codes=k_codes,
+                  k_scale=k_scale, k_bscale=None, v_packed=v_packed, v_scales=v_scales,
+                  centroids=pk.GAUSSIAN_3BIT.centroids, sign_seed=None, status=status, replay=None, device=dev)
+    torch.cuda.synchronize()
+    assert intact(), "pkv_encode wrote outside its documented outputs"
+    for li in range(L):  # and the codes are the reference's
+        s, kc = O.quantize_k_tensor(ks[li].float().cpu().numpy())
+        vc, vsc = O.quantize_v(vs[li].float().cpu().numpy().reshape(1, H, T, D))
+        assert np.array_equal(k_codes[li].cpu().numpy(), kc.reshape(-1))
+        assert bytes(v_packed[li].cpu().numpy()) == O.pack3(vc)
+    for out_dt, eb in ((torch.bfloat16, 2), (torch.float32, 4)):
+        outs, intact_o = _canary_views([n * eb] * (2 * L), [out_dt] * (2 * L), dev)
+        _codec.decode(num_vectors=nvec, head_dim=D, out_dtype=out_dt, k_mode=K_MODES["tensor"], k_codes=k_codes,
+                      k_scale=k_scale, k_bscale=None, v_packed=v_packed, v_scales=v_scales,
+                      centroids=pk.GAUSSIAN_3BIT.centroids, sign_seed=None, k_out=outs[:L], v_out=outs[L:],
+                      device=dev)
+        torch.cuda.synchronize()
+        assert intact_o(), f"pkv_decode ({out_dt}) wrote outside its outputs"
+
+
+@pytest.mark.parametrize("D,H,T", [(128, 3, 37), (64, 2, 5), (4, 3, 11)])
+def test_block32_encode_writes_exactly_the_documented_bytes(D, H, T):
+    from paper_2604_24971_b200 import _codec
+    from paper_2604_24971_b200.keyquant import K_MODES
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = H * T * D
+    ks = [torch.from_numpy(np.random.default_rng(T).normal(size=n).astype(np.float32)).to(dev)]
+    nb = (n + 31) // 32
+    (k_codes, k_bscale), intact = _canary_views([n, 2 * nb], [torch.int8, torch.int16], dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _codec.encode(num_vectors=H * T, head_dim=D, k_in=ks, v_in=None, k_mode=K_MODES["block32"], k_codes=[k_codes],
+                  k_scale=None, k_bscale=[k_bscale], v_packed=None, v_scales=None,
+                  centroids=pk.GAUSSIAN_3BIT.centroids, sign_seed=None, status=status, replay=None, device=dev)
+    torch.cuda.synchronize()
+    assert intact(), "block32 pkv_encode wrote outside its documented outputs"
+    s16, kc = O.quantize_k_block32(ks[0].cpu().numpy())
+    assert np.array_equal(k_codes.cpu().numpy(), kc) and np.array_equal(k_bscale.cpu().numpy().view(np.uint16), s16.view(np.uint16))
