@@ -555,3 +555,27 @@ def test_block32_encode_writes_exactly_the_documented_bytes(D, H, T):
     assert intact(), "block32 pkv_encode wrote outside its documented outputs"
     s16, kc = O.quantize_k_block32(ks[0].cpu().numpy())
     assert np.array_equal(k_codes.cpu().numpy(), kc) and np.array_equal(k_bscale.cpu().numpy().view(np.uint16), s16.view(np.uint16))
+
+
+@pytest.mark.parametrize("D,H,T,R,G,cap", [(128, 8, 1000, 15, 4, 16), (64, 4, 70, 3, 2, 0), (128, 2, 5, 1, 1, 3)])
+def test_attention_writes_exactly_its_output_and_workspace(D, H, T, R, G, cap):
+    from paper_2604_24971_b200 import _lib
+    from paper_2604_24971_b200 import attention as A
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = pk.ModelGeometry(num_layers=1, kv_heads=H, head_dim=D, seq_len=T)
+    pool = pk.build_pool(pk.synth_gaussian_dump(g, seed=T, device=dev), build_stats=False)
+    need = _lib.load().pkv_attention_workspace_bytes(R, H, G, D, T)
+    (out, ws), intact = _canary_views([R * H * G * D * 4, ((need + 3) // 4) * 4], [torch.float32, torch.float32], dev)
+    gen = torch.Generator(device="cuda").manual_seed(T)
+    q = torch.randn(R, H, G, D, device=dev, generator=gen)
+    kw = {}
+    if cap:
+        kw = dict(tail_k=torch.randn(R, H, cap, D, device=dev, generator=gen).bfloat16(),
+                  tail_v=torch.randn(R, H, cap, D, device=dev, generator=gen).bfloat16(),
+                  tail_len=torch.randint(0, cap + 1, (R,), device=dev, dtype=torch.int32, generator=gen))
+    res = A.decode_attention(pool, 0, q, out=out.view(R, H, G, D), workspace=ws, out_dtype=torch.float32, **kw)
+    torch.cuda.synchronize()
+    assert res.data_ptr() == out.data_ptr()
+    assert intact(), "decode attention wrote outside its output / workspace"
+    assert bool(torch.isfinite(res).all())
